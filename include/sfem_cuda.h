@@ -1,0 +1,112 @@
+/* sfem_cuda.h -- C-ABI of the B200-native spectral FEM Poisson solver.
+ *
+ * Drop-in boundary for the reference's hot path (algorithm (a), full
+ * diagonalisation, and the standalone 1D expand/unexpand).  Plain pointers and
+ * sizes only; every entry point returns 0 on success and a nonzero status
+ * otherwise, with the message (the reference's sfem::Error text where one
+ * exists) available from sfem_cuda_last_error() on the calling thread.
+ * No C++ exception crosses this boundary (reference: types.hpp:9-18 throws
+ * sfem::Error everywhere; include/sfem_b200.hpp rethrows it on the C++ side).
+ *
+ * Data layout ("dof layout"): an N-D grid function or coefficient tensor is
+ * one dense FP64 array, row-major, last axis fastest, with per-axis extent
+ * L_i = n_i*K_i - 1 in the interleaved dof order of the reference's dense
+ * oracle (dof t = e*n + c: interior component c of element e; t = j*n - 1:
+ * node j; reference proj/src/banded.cpp:9-15, oracle.cpp:64-144).  Device
+ * tensors may pad the last axis to a pitch (in elements) >= L_{N-1}.
+ * Coefficients of an axis are in the reference's frequency-major order
+ * (grid1d.hpp:41-58).
+ */
+#ifndef SFEM_CUDA_H
+#define SFEM_CUDA_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sfem_ctx_s* sfem_ctx;     /* device + stream                 */
+typedef struct sfem_table_s* sfem_table; /* spectral table for one (n, K)   */
+typedef struct sfem_plan_s* sfem_plan;   /* algorithm (a) solve plan        */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int sfem_cuda_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* sfem_cuda_last_error(void);
+
+/* Context on CUDA device `device` with its own stream.
+ * Replaces the implicit process state of the reference (OpenMP pool,
+ * FFTW plan cache: trig.cpp:27-67, poisson.cpp:81-87). */
+int sfem_cuda_ctx_create(int device, sfem_ctx* out);
+int sfem_cuda_ctx_destroy(sfem_ctx ctx);
+/* The context's stream as a cudaStream_t (void*). */
+int sfem_cuda_ctx_stream(sfem_ctx ctx, void** stream);
+
+/* Spectral table for order n (1..9) and K >= 2 elements, built on the host
+ * and uploaded.  Replaces TableSet::get / build_spectral_table
+ * (reference poisson.hpp:54, spectral.hpp:316). */
+int sfem_cuda_table_create(sfem_ctx ctx, int order, int elements, sfem_table* out);
+int sfem_cuda_table_destroy(sfem_table table);
+/* Host copies of the table's primaries (SpectralTable1D fields, spectral.hpp:281-312).
+ * Any pointer may be NULL.  Sizes: values/norm_sq (K-1)*n; p (K-1)*n*(n-1);
+ * interior_values n-1; interior_vectors (n-1)^2 row-major [i][l-1];
+ * eig_coeff n*K-1 (eigenvalues_coeff_order, spectral.cpp:10-17). */
+int sfem_cuda_table_export(sfem_table table, double* values, double* norm_sq, double* p,
+                           double* interior_values, double* interior_vectors, double* eig_coeff);
+
+/* 1D line operations (reference eigenbasis.hpp:50-79):
+ *   SFEM_OP_DECOMPOSE_WEIGHTED  lines::decompose_weighted  (FC_n, eigenbasis.cpp:63-101)
+ *   SFEM_OP_DECOMPOSE           lines::decompose           (F_n,  eigenbasis.cpp:103-142)
+ *   SFEM_OP_SYNTHESIZE          lines::synthesize          (F_n^-1, eigenbasis.cpp:144-225)
+ * on `count` lines of length L = n*K-1, line b at in + b*in_pitch (dof layout
+ * for the analyses, coefficient layout for synthesis).  In-place allowed when
+ * in == out and the pitches agree. */
+enum { SFEM_OP_DECOMPOSE_WEIGHTED = 0, SFEM_OP_DECOMPOSE = 1, SFEM_OP_SYNTHESIZE = 2 };
+int sfem_cuda_lines_device(sfem_table table, int op, long long count, const double* d_in,
+                           long long in_pitch, double* d_out, long long out_pitch, void* stream);
+/* Same on host buffers (dense, pitch = L); host<->device copies included. */
+int sfem_cuda_lines_host(sfem_table table, int op, long long count, const double* h_in, double* h_out);
+
+/* Solve plan for  -sum_i a_i d^2u/dx_i^2 + shift*u = f  on the box
+ * prod [0, lengths_i] with homogeneous Dirichlet data, orders n_i and K_i
+ * elements per axis (reference ProblemSpec, poisson.hpp:29-41; a_i = 1 there).
+ * `coefficients` may be NULL (all ones).  Validation and the nonpositive-
+ * symbol check follow ProblemSpec::validate (poisson.cpp:32-47) and
+ * detail::scale_by_symbol (poisson.cpp:573-631), with their messages.
+ * dim 1..4. */
+int sfem_cuda_plan_create(sfem_ctx ctx, int dim, const int* orders, const int* elements,
+                          const double* lengths, const double* coefficients, double shift, sfem_plan* out);
+int sfem_cuda_plan_destroy(sfem_plan plan);
+/* Extents L_i (dim entries), default device pitch of the last axis, total unknowns. */
+int sfem_cuda_plan_shape(sfem_plan plan, long long* extents, long long* pitch, long long* unknowns);
+/* Kernel launches per solve (2N-1 for the fused schedule). */
+int sfem_cuda_plan_launches(sfem_plan plan, int* launches);
+
+/* Device-resident solve, in place: d_data holds the load (dof layout, last
+ * axis padded to `pitch` elements) and receives u.  Replaces
+ * solve_with_load's timed core run_full_diagonalization (poisson.cpp:637-669,
+ * timed region 781-785).  stream NULL = the context stream. */
+int sfem_cuda_solve_device(sfem_plan plan, double* d_data, long long pitch, void* stream);
+
+/* Host solve: dense dof-layout load in, dense u out (h_u may equal h_load).
+ * Host->device and device->host copies are inside.  `seconds` (may be NULL)
+ * receives the device-timed solve alone (SolveReport::seconds_solve). */
+int sfem_cuda_solve_host(sfem_plan plan, const double* h_load, double* h_u, double* seconds);
+
+/* Host solve in the reference's GridFunctionND layout (ndgrid.hpp:43-57): 2^dim
+ * class arrays, mask bit i set = element-interior indexing on axis i, class
+ * extents K_i+1 (nodal, boundary slots included) or K_i*(n_i-1); row-major.
+ * Boundary slots of the result are zero (enforce_boundary, ndgrid.cpp:34-45). */
+int sfem_cuda_solve_classes(sfem_plan plan, const double* const* h_load_classes, double* const* h_u_classes,
+                            double* seconds);
+
+/* Timing helper for benchmarks: `reps` solves of d_data back to back on the
+ * plan stream, bracketed by CUDA events; per-sweep-kernel times (ms, averaged
+ * over reps) into kernel_ms[0 .. launches-1] when non-NULL. */
+int sfem_cuda_solve_device_timed(sfem_plan plan, double* d_data, long long pitch, int reps, double* total_ms,
+                                 double* kernel_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,450 @@
+"""paper_1701_03967_b200 -- B200-native FP64 fast spectral solver for the
+tensor-product n-th order FEM generalized Poisson equation (arXiv 1701.03967).
+
+Host-side mirror of the reference's C++ solver API (reference
+proj/include/sfem/poisson.hpp, eigenbasis.hpp, grid1d.hpp, ndgrid.hpp) over the
+C-ABI in include/sfem_cuda.h.  Every numeric operation runs in the in-tree CUDA
+library libsfem_b200.so; there is no CPU fallback: importing on a machine
+without the library raises ImportError, and calls without a CUDA device raise
+Error from the library.
+
+Names, argument meaning and error behaviour follow the reference:
+  ProblemSpec, SolveOptions, SolveReport, TableSet, solve_with_load,
+  GridFunctionND, GridFunction1D, CoefficientArray1D,
+  synthesize / decompose / decompose_weighted (+ batched line forms),
+  Error (the reference's sfem::Error).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "Error", "lib", "lib_path", "Context", "SpectralTable", "TableSet", "ProblemSpec", "SolveOptions",
+    "SolveReport", "Plan", "GridFunction1D", "CoefficientArray1D", "GridFunctionND", "solve_with_load",
+    "solve_dof", "synthesize", "decompose", "decompose_weighted", "lines", "DECOMPOSE_WEIGHTED",
+    "DECOMPOSE", "SYNTHESIZE", "default_context", "HEADER_SYMBOLS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libsfem_b200.so")
+
+DECOMPOSE_WEIGHTED, DECOMPOSE, SYNTHESIZE = 0, 1, 2
+
+
+class Error(RuntimeError):
+    """Mirror of sfem::Error (reference types.hpp:9-18)."""
+
+
+def _load():
+    if not os.path.exists(lib_path):
+        raise ImportError(
+            f"paper_1701_03967_b200: CUDA library missing at {lib_path}; run __graft_entry__.build() "
+            "(there is no CPU fallback)")
+    return ctypes.CDLL(lib_path)
+
+
+lib = _load()
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+_llp = ctypes.POINTER(ctypes.c_longlong)
+_vp = ctypes.c_void_p
+
+# (name, restype, argtypes) for every entry point in include/sfem_cuda.h
+_SIGS = [
+    ("sfem_cuda_version", ctypes.c_int, []),
+    ("sfem_cuda_last_error", ctypes.c_char_p, []),
+    ("sfem_cuda_ctx_create", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_ctx_destroy", ctypes.c_int, [_vp]),
+    ("sfem_cuda_ctx_stream", ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_table_create", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_table_destroy", ctypes.c_int, [_vp]),
+    ("sfem_cuda_table_export", ctypes.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    ("sfem_cuda_lines_device", ctypes.c_int,
+     [_vp, ctypes.c_int, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp]),
+    ("sfem_cuda_lines_host", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_longlong, _dp, _dp]),
+    ("sfem_cuda_plan_create", ctypes.c_int,
+     [_vp, ctypes.c_int, _ip, _ip, _dp, _dp, ctypes.c_double, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_plan_destroy", ctypes.c_int, [_vp]),
+    ("sfem_cuda_plan_shape", ctypes.c_int, [_vp, _llp, _llp, _llp]),
+    ("sfem_cuda_plan_launches", ctypes.c_int, [_vp, _ip]),
+    ("sfem_cuda_solve_device", ctypes.c_int, [_vp, _vp, ctypes.c_longlong, _vp]),
+    ("sfem_cuda_solve_host", ctypes.c_int, [_vp, _dp, _dp, _dp]),
+    ("sfem_cuda_solve_classes", ctypes.c_int, [_vp, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _dp]),
+    ("sfem_cuda_solve_device_timed", ctypes.c_int,
+     [_vp, _vp, ctypes.c_longlong, ctypes.c_int, _dp, _dp]),
+]
+HEADER_SYMBOLS = [s[0] for s in _SIGS]
+for _name, _res, _args in _SIGS:
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def _check(status: int):
+    if status != 0:
+        raise Error(lib.sfem_cuda_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Context:
+    """A CUDA device with its stream (sfem_cuda_ctx_create)."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(lib.sfem_cuda_ctx_create(device, ctypes.byref(h)))
+        self.handle = h
+        self.device = device
+
+    @property
+    def stream(self) -> int:
+        s = _vp()
+        _check(lib.sfem_cuda_ctx_stream(self.handle, ctypes.byref(s)))
+        return s.value or 0
+
+    def close(self):
+        if self.handle:
+            lib.sfem_cuda_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_DEFAULT: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Context(int(os.environ.get("SFEM_DEVICE", "0")))
+    return _DEFAULT
+
+
+class SpectralTable:
+    """Device spectral table for one (order, elements) (SpectralTable1D, spectral.hpp:281-312)."""
+
+    def __init__(self, order: int, elements: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        h = _vp()
+        _check(lib.sfem_cuda_table_create(self.ctx.handle, order, elements, ctypes.byref(h)))
+        self.handle = h
+        self.order = order
+        self.elements = elements
+
+    @property
+    def coeff_count(self) -> int:
+        return self.order * self.elements - 1
+
+    def export(self) -> dict:
+        n, K = self.order, self.elements
+        m = n - 1
+        out = dict(values=np.empty((K - 1) * n), norm_sq=np.empty((K - 1) * n),
+                   p=np.empty(max(1, (K - 1) * n * m)), interior_values=np.empty(max(1, m)),
+                   interior_vectors=np.empty(max(1, m * m)), eig_coeff=np.empty(n * K - 1))
+        _check(lib.sfem_cuda_table_export(self.handle, *[_dptr(out[k]) for k in
+                                                         ("values", "norm_sq", "p", "interior_values",
+                                                          "interior_vectors", "eig_coeff")]))
+        out["p"] = out["p"][:(K - 1) * n * m]
+        out["interior_values"] = out["interior_values"][:m]
+        out["interior_vectors"] = out["interior_vectors"][:m * m]
+        return out
+
+    def eigenvalues_coeff_order(self) -> np.ndarray:
+        return self.export()["eig_coeff"]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.sfem_cuda_table_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+class TableSet:
+    """Tables keyed by (order, elements), built on demand (TableSet, poisson.hpp:48-62)."""
+
+    def __init__(self, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self._tables = {}
+
+    def get(self, order: int, elements: int) -> SpectralTable:
+        key = (order, elements)
+        if key not in self._tables:
+            self._tables[key] = SpectralTable(order, elements, self.ctx)
+        return self._tables[key]
+
+
+# ---------------------------------------------------------------------------
+# 1D data types (grid1d.hpp:13-61) and the 1D API (eigenbasis.hpp:76-79)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class GridFunction1D:
+    order: int
+    elements: int
+    nodal: np.ndarray      # K+1, boundary entries zero
+    interior: np.ndarray   # K*(n-1), element-major
+
+    @staticmethod
+    def zeros(n: int, K: int) -> "GridFunction1D":
+        return GridFunction1D(n, K, np.zeros(K + 1), np.zeros(K * (n - 1)))
+
+    def to_dof(self) -> np.ndarray:
+        n, K = self.order, self.elements
+        full = np.zeros((K, n))
+        full[:, :n - 1] = self.interior.reshape(K, n - 1)
+        full[:K - 1, n - 1] = self.nodal[1:K]
+        return full.reshape(-1)[:n * K - 1].copy()
+
+    @staticmethod
+    def from_dof(v: np.ndarray, n: int, K: int) -> "GridFunction1D":
+        full = np.concatenate([np.asarray(v, float), [0.0]]).reshape(K, n)
+        nodal = np.zeros(K + 1)
+        nodal[1:K] = full[:K - 1, n - 1]
+        return GridFunction1D(n, K, nodal, full[:, :n - 1].reshape(-1).copy())
+
+    def dof_count(self) -> int:
+        return self.order * self.elements - 1
+
+
+@dataclass
+class CoefficientArray1D:
+    order: int
+    elements: int
+    data: np.ndarray  # n*K-1, frequency-major
+
+    @staticmethod
+    def zeros(n: int, K: int) -> "CoefficientArray1D":
+        return CoefficientArray1D(n, K, np.zeros(n * K - 1))
+
+    def index(self, k: int, l: int) -> int:
+        return l - 1 if k == 0 else (self.order - 1) + (k - 1) * self.order + (l - 1)
+
+    def at(self, k: int, l: int) -> float:
+        return float(self.data[self.index(k, l)])
+
+
+def lines(table: SpectralTable, op: int, x: np.ndarray) -> np.ndarray:
+    """Batched line transform on host arrays of shape (count, n*K-1) (lines::*, eigenbasis.hpp:50-73)."""
+    x = _f64(x)
+    L = table.coeff_count
+    if x.ndim == 1:
+        x = x.reshape(1, -1)
+    if x.shape[-1] != L:
+        raise Error(f"lines: line length {x.shape[-1]} does not match the table (n*K-1 = {L})")
+    out = np.empty_like(x)
+    _check(lib.sfem_cuda_lines_host(table.handle, op, x.shape[0], _dptr(x), _dptr(out)))
+    return out
+
+
+def synthesize(coeffs: CoefficientArray1D, table: SpectralTable) -> GridFunction1D:
+    """eigenbasis.cpp:448-455."""
+    if coeffs.order != table.order or coeffs.elements != table.elements:
+        raise Error("synthesize: coefficient array does not match the table")
+    v = lines(table, SYNTHESIZE, coeffs.data)[0]
+    return GridFunction1D.from_dof(v, table.order, table.elements)
+
+
+def decompose_weighted(y: GridFunction1D, table: SpectralTable) -> CoefficientArray1D:
+    """eigenbasis.cpp:457-464."""
+    if y.order != table.order or y.elements != table.elements:
+        raise Error("decompose_weighted: grid function does not match the table")
+    return CoefficientArray1D(table.order, table.elements, lines(table, DECOMPOSE_WEIGHTED, y.to_dof())[0])
+
+
+def decompose(w: GridFunction1D, table: SpectralTable) -> CoefficientArray1D:
+    """eigenbasis.cpp:466-475 (Spectral route)."""
+    if w.order != table.order or w.elements != table.elements:
+        raise Error("decompose: grid function does not match the table")
+    return CoefficientArray1D(table.order, table.elements, lines(table, DECOMPOSE, w.to_dof())[0])
+
+
+# ---------------------------------------------------------------------------
+# N-D problem and solve (poisson.hpp:29-91, ndgrid.hpp:18-57)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ProblemSpec:
+    """ProblemSpec (poisson.hpp:29-41) plus per-axis diffusion coefficients a_i (default 1)."""
+    dimension: int
+    lengths: Sequence[float]
+    elements: Sequence[int]
+    orders: Sequence[int]
+    shift: float = 0.0
+    coefficients: Optional[Sequence[float]] = None
+
+    def shift_lower_bound(self) -> float:
+        a = self.coefficients or [1.0] * self.dimension
+        return -np.pi ** 2 * sum(ai / (x * x) for ai, x in zip(a, self.lengths))
+
+    def extents(self) -> List[int]:
+        return [n * K - 1 for n, K in zip(self.orders, self.elements)]
+
+    def validate(self):
+        """poisson.cpp:32-47 (messages and order of checks)."""
+        if self.dimension < 1:
+            raise Error("problem: dimension must be at least 1")
+        if not (len(self.lengths) == len(self.elements) == len(self.orders) == self.dimension):
+            raise Error("problem: lengths/elements/orders must all have `dimension` entries")
+        for i in range(self.dimension):
+            if not self.lengths[i] > 0:
+                raise Error(f"problem: box length must be positive (axis {i + 1})")
+            if self.elements[i] < 2:
+                raise Error(f"problem: need at least 2 elements (axis {i + 1})")
+            if not (1 <= self.orders[i] <= 9):
+                raise Error(f"problem: order out of range (axis {i + 1})")
+        if not self.shift > self.shift_lower_bound():
+            raise Error(f"problem: shift {self.shift:f} must exceed {self.shift_lower_bound():f} "
+                        "for a positive definite operator")
+
+
+@dataclass
+class SolveOptions:
+    """SolveOptions (poisson.hpp:64-70); only FullDiagonalization runs on the GPU path."""
+    algorithm: str = "full"
+    threads: int = 0
+    compute_residual: bool = False
+    tables: Optional[TableSet] = None
+
+
+@dataclass
+class GridFunctionND:
+    """2^N parity-class arrays (ndgrid.hpp:43-57): mask bit i = interior indexing on axis i."""
+    orders: Sequence[int]
+    elements: Sequence[int]
+    classes: List[np.ndarray] = field(default_factory=list)
+
+    def class_extents(self, mask: int) -> List[int]:
+        return [(K * (n - 1)) if (mask >> i) & 1 else K + 1
+                for i, (n, K) in enumerate(zip(self.orders, self.elements))]
+
+    @staticmethod
+    def zeros(orders, elements) -> "GridFunctionND":
+        g = GridFunctionND(list(orders), list(elements))
+        g.classes = [np.zeros(g.class_extents(mask)) for mask in range(1 << len(orders))]
+        return g
+
+
+@dataclass
+class SolveReport:
+    """SolveReport (poisson.hpp:72-78)."""
+    solution: object
+    seconds_solve: float = 0.0
+    seconds_load: float = 0.0
+    residual_rel: Optional[float] = None
+    error_uniform: Optional[float] = None
+
+
+class Plan:
+    """A device solve plan (sfem_cuda_plan_create) for one ProblemSpec."""
+
+    def __init__(self, spec: ProblemSpec, ctx: Optional[Context] = None):
+        spec.validate()
+        self.ctx = ctx or default_context()
+        self.spec = spec
+        N = spec.dimension
+        orders = (ctypes.c_int * N)(*spec.orders)
+        elements = (ctypes.c_int * N)(*spec.elements)
+        lengths = (ctypes.c_double * N)(*spec.lengths)
+        coeffs = (ctypes.c_double * N)(*spec.coefficients) if spec.coefficients is not None else None
+        h = _vp()
+        _check(lib.sfem_cuda_plan_create(self.ctx.handle, N, orders, elements, lengths,
+                                         ctypes.cast(coeffs, _dp) if coeffs is not None else None,
+                                         float(spec.shift), ctypes.byref(h)))
+        self.handle = h
+        ext = (ctypes.c_longlong * N)()
+        pitch = ctypes.c_longlong()
+        unk = ctypes.c_longlong()
+        _check(lib.sfem_cuda_plan_shape(h, ext, ctypes.byref(pitch), ctypes.byref(unk)))
+        self.extents = list(ext)
+        self.pitch = pitch.value
+        self.unknowns = unk.value
+        nl = ctypes.c_int()
+        _check(lib.sfem_cuda_plan_launches(h, ctypes.byref(nl)))
+        self.launches = nl.value
+
+    @property
+    def padded_shape(self):
+        return tuple(self.extents[:-1]) + (self.pitch,)
+
+    def solve_host(self, load: np.ndarray):
+        load = _f64(load)
+        if list(load.shape) != self.extents:
+            raise Error(f"solve: load shape {list(load.shape)} does not match the dof extents {self.extents}")
+        u = np.empty_like(load)
+        sec = ctypes.c_double()
+        _check(lib.sfem_cuda_solve_host(self.handle, _dptr(load), _dptr(u), ctypes.byref(sec)))
+        return u, sec.value
+
+    def solve_device(self, dev_ptr: int, pitch: Optional[int] = None, stream: int = 0):
+        _check(lib.sfem_cuda_solve_device(self.handle, ctypes.c_void_p(dev_ptr),
+                                          self.pitch if pitch is None else pitch, ctypes.c_void_p(stream or None)))
+
+    def solve_device_timed(self, dev_ptr: int, reps: int, pitch: Optional[int] = None):
+        total = ctypes.c_double()
+        per = (ctypes.c_double * self.launches)()
+        _check(lib.sfem_cuda_solve_device_timed(self.handle, ctypes.c_void_p(dev_ptr),
+                                                self.pitch if pitch is None else pitch, reps,
+                                                ctypes.byref(total), per))
+        return total.value, list(per)
+
+    def solve_classes(self, load: GridFunctionND) -> GridFunctionND:
+        N = self.spec.dimension
+        ins = [_f64(c) for c in load.classes]
+        out = GridFunctionND.zeros(self.spec.orders, self.spec.elements)
+        in_arr = (_dp * (1 << N))(*[_dptr(c) for c in ins])
+        out_arr = (_dp * (1 << N))(*[_dptr(c) for c in out.classes])
+        sec = ctypes.c_double()
+        _check(lib.sfem_cuda_solve_classes(self.handle, in_arr, out_arr, ctypes.byref(sec)))
+        return out, sec.value
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.sfem_cuda_plan_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def solve_dof(spec: ProblemSpec, load: np.ndarray, ctx: Optional[Context] = None):
+    """Solve on a dense dof-layout load tensor; returns (u, seconds_solve)."""
+    return Plan(spec, ctx).solve_host(load)
+
+
+def solve_with_load(spec: ProblemSpec, load, tables: Optional[TableSet] = None,
+                    options: Optional[SolveOptions] = None) -> SolveReport:
+    """solve_with_load (poisson.hpp:90-91; poisson.cpp:771-794), algorithm (a).
+
+    `load` is either a GridFunctionND (the reference layout) or a dense dof
+    tensor; the solution comes back in the same form.  `tables` is accepted for
+    interface parity (device tables are owned by the plan)."""
+    options = options or SolveOptions()
+    if options.algorithm != "full":
+        raise Error("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path")
+    ctx = tables.ctx if tables is not None else None
+    plan = Plan(spec, ctx)
+    if isinstance(load, GridFunctionND):
+        sol, sec = plan.solve_classes(load)
+    else:
+        sol, sec = plan.solve_host(load)
+    return SolveReport(solution=sol, seconds_solve=sec)

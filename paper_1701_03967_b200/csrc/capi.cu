@@ -1,0 +1,687 @@
+// C-ABI implementation (include/sfem_cuda.h): contexts, device tables, solve
+// plans and the sweep schedule of algorithm (a).
+//
+// Schedule for an N-D solve on a dof tensor (reference run_full_diagonalization,
+// poisson.cpp:637-669, which sweeps forward 0..N-1, divides, then inverts
+// N-1..0):
+//   forward sweeps along axes 0..N-2            (strided lines, tiles of B
+//                                                 adjacent lines)
+//   one fused sweep along the last axis:        forward + symbol divide +
+//                                                 inverse, data never leaves
+//                                                 shared memory in between
+//   inverse sweeps along axes N-2..0
+// = 2N-1 launches and 2N-1 passes over HBM instead of 2N.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sfem_cuda.h"
+#include "sweep.cuh"
+#include "table.hpp"
+
+using namespace sfem_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  } catch (...) {
+    g_err = "unknown error";
+    return 1;
+  }
+}
+
+[[noreturn]] void fail(const std::string& msg) { throw std::runtime_error(msg); }
+void require(bool c, const std::string& msg) {
+  if (!c) fail(msg);
+}
+
+std::vector<int> factor_radices(int N) {
+  std::vector<int> r;
+  int m = N;
+  while (m % 4 == 0) {
+    r.push_back(4);
+    m /= 4;
+  }
+  while (m % 2 == 0) {
+    r.push_back(2);
+    m /= 2;
+  }
+  for (int p = 3; m > 1; p += 2)
+    while (m % p == 0) {
+      r.push_back(p);
+      m /= p;
+    }
+  return r;
+}
+
+constexpr size_t kSmemMax = 227 * 1024;
+
+}  // namespace
+
+struct sfem_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+};
+
+struct sfem_table_s {
+  sfem_ctx ctx = nullptr;
+  HostTable host;
+  double* dbuf = nullptr;
+  DevTable dev{};
+};
+
+namespace {
+
+void upload_table(sfem_table_s* t) {
+  const DeviceTableData d = derive_device_data(t->host);
+  std::vector<const std::vector<double>*> parts = {&d.mix_fwd_w, &d.mix_fwd_d, &d.mix_inv, &d.e0_fwd_w,
+                                                   &d.e0_fwd_d,  &d.e0_inv,    &d.eig,     &d.tw,
+                                                   &d.mk,        &d.mkh,       &d.om};
+  std::vector<size_t> offs;
+  size_t total = 0;
+  for (const auto* p : parts) {
+    offs.push_back(total);
+    total += (p->size() + 1) & ~static_cast<size_t>(1);  // keep 16-byte alignment
+  }
+  std::vector<double> packed(total, 0.0);
+  for (size_t i = 0; i < parts.size(); ++i)
+    std::copy(parts[i]->begin(), parts[i]->end(), packed.begin() + offs[i]);
+  ck(cudaSetDevice(t->ctx->device), "cudaSetDevice");
+  ck(cudaMalloc(&t->dbuf, std::max<size_t>(total, 2) * sizeof(double)), "cudaMalloc(table)");
+  ck(cudaMemcpy(t->dbuf, packed.data(), total * sizeof(double), cudaMemcpyHostToDevice), "upload table");
+  DevTable& v = t->dev;
+  v.n = d.n;
+  v.K = d.K;
+  v.m = d.n - 1;
+  v.half = v.m / 2;
+  v.ne = d.n / 2;
+  v.L = d.n * d.K - 1;
+  v.mix_fwd_w = t->dbuf + offs[0];
+  v.mix_fwd_d = t->dbuf + offs[1];
+  v.mix_inv = t->dbuf + offs[2];
+  v.e0_fwd_w = t->dbuf + offs[3];
+  v.e0_fwd_d = t->dbuf + offs[4];
+  v.e0_inv = t->dbuf + offs[5];
+  v.eig = t->dbuf + offs[6];
+  v.tw = reinterpret_cast<const double2*>(t->dbuf + offs[7]);
+  v.mk = reinterpret_cast<const double2*>(t->dbuf + offs[8]);
+  v.mkh = reinterpret_cast<const double2*>(t->dbuf + offs[9]);
+  v.om = reinterpret_cast<const double2*>(t->dbuf + offs[10]);
+  const std::vector<int> r = factor_radices(d.K);
+  require(static_cast<int>(r.size()) <= kMaxPasses, "table: too many FFT passes");
+  v.npass = static_cast<int>(r.size());
+  for (size_t i = 0; i < r.size(); ++i) v.radix[i] = r[i];
+}
+
+// Largest tile (lines per CTA) that fits shared memory; prefer two CTAs/SM.
+int choose_tile(const DevTable& t, long long nlines) {
+  const int cands[] = {16, 8, 4, 2, 1};
+  for (int B : cands) {
+    if (B > 1 && B > nlines) continue;
+    if (sweep_smem_bytes(t, B) <= kSmemMax / 2) return B;
+  }
+  for (int B : cands) {
+    if (B > 1 && B > nlines) continue;
+    if (sweep_smem_bytes(t, B) <= kSmemMax) return B;
+  }
+  fail("sfem_cuda: line length " + std::to_string(t.L) + " (n=" + std::to_string(t.n) + ", K=" +
+       std::to_string(t.K) + ") exceeds the shared-memory tile of this build");
+}
+
+struct Step {
+  int axis;
+  int mode;
+  LineSet ls;  // src/dst filled at launch
+  int B;
+  SymbolInfo sym;
+};
+
+}  // namespace
+
+struct sfem_plan_s {
+  sfem_ctx ctx = nullptr;
+  int dim = 0;
+  std::vector<int> orders, elements;
+  std::vector<double> lengths, coeffs, factors;
+  double shift = 0;
+  std::vector<std::unique_ptr<sfem_table_s>> owned;
+  std::vector<sfem_table_s*> tables;  // per axis
+  std::vector<long long> ext;
+  long long pitch = 0;
+  long long rows = 0;  // product of leading extents
+  std::vector<Step> steps;
+  double* dwork = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> kev;
+};
+
+namespace {
+
+void build_steps(sfem_plan_s* p, long long pitch) {
+  const int N = p->dim;
+  std::vector<long long> st(N);
+  st[N - 1] = 1;
+  if (N >= 2) st[N - 2] = pitch;
+  for (int i = N - 3; i >= 0; --i) st[i] = st[i + 1] * p->ext[i + 1];
+  p->steps.clear();
+  auto strided = [&](int a, int mode) {
+    Step s{};
+    s.axis = a;
+    s.mode = mode;
+    LineSet& ls = s.ls;
+    ls.ninner = p->ext[N - 1];
+    ls.is = 1;
+    std::vector<int> outer;
+    for (int i = 0; i < N - 1; ++i)
+      if (i != a) outer.push_back(i);
+    ls.n1 = 1;
+    ls.os1 = 0;
+    ls.os2 = 0;
+    if (outer.size() >= 1) {
+      ls.n1 = p->ext[outer.back()];
+      ls.os1 = st[outer.back()];
+    }
+    if (outer.size() == 2) ls.os2 = st[outer[0]];
+    long long nl = ls.ninner;
+    for (int i : outer) nl *= p->ext[i];
+    ls.nlines = nl;
+    ls.ps = st[a];
+    ls.contiguous = 0;
+    s.B = choose_tile(p->tables[a]->dev, nl);
+    p->steps.push_back(s);
+  };
+  for (int a = 0; a < N - 1; ++a) strided(a, kForward);
+  {
+    Step s{};
+    s.axis = N - 1;
+    s.mode = kForwardDivideInverse;
+    LineSet& ls = s.ls;
+    ls.nlines = p->rows;
+    ls.ninner = 1;
+    ls.n1 = p->rows;
+    ls.is = 0;
+    ls.os1 = pitch;
+    ls.os2 = 0;
+    ls.ps = 1;
+    ls.contiguous = 1;
+    SymbolInfo& sy = s.sym;
+    sy.nlead = N - 1;
+    for (int i = 0; i < N - 1; ++i) {
+      sy.lead_ext[i] = p->ext[i];
+      sy.lead_eig[i] = p->tables[i]->dev.eig;
+      sy.lead_f[i] = p->factors[i];
+    }
+    sy.shift = p->shift;
+    sy.f_last = p->factors[N - 1];
+    s.B = choose_tile(p->tables[N - 1]->dev, ls.nlines);
+    p->steps.push_back(s);
+  }
+  for (int a = N - 2; a >= 0; --a) strided(a, kInverse);
+}
+
+void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
+  if (pitch != p->pitch) build_steps(p, pitch), p->pitch = pitch;
+  for (size_t i = 0; i < p->steps.size(); ++i) {
+    Step s = p->steps[i];
+    s.ls.src = data;
+    s.ls.dst = data;
+    if (events) ck(cudaEventRecord(p->kev[i], stream), "event");
+    ck(launch_sweep(p->tables[s.axis]->dev, s.ls, s.mode, kWeighted, s.mode == kForwardDivideInverse ? &s.sym : nullptr,
+                    s.B, stream),
+       "sweep launch");
+  }
+  if (events) ck(cudaEventRecord(p->kev[p->steps.size()], stream), "event");
+}
+
+// Reference ProblemSpec::validate (poisson.cpp:32-47), with per-axis coefficients.
+void validate(int dim, const int* orders, const int* elements, const double* lengths, const double* coeffs,
+              double shift) {
+  require(dim >= 1, "problem: dimension must be at least 1");
+  require(dim <= kMaxDim, "problem: dimension above " + std::to_string(kMaxDim) + " is not supported by this build");
+  double bound = 0;
+  for (int i = 0; i < dim; ++i) {
+    require(lengths[i] > 0, "problem: box length must be positive (axis " + std::to_string(i + 1) + ")");
+    require(elements[i] >= 2, "problem: need at least 2 elements (axis " + std::to_string(i + 1) + ")");
+    require(orders[i] >= 1 && orders[i] <= 9, "problem: order out of range (axis " + std::to_string(i + 1) + ")");
+    const double a = coeffs ? coeffs[i] : 1.0;
+    require(a > 0, "problem: diffusion coefficient must be positive (axis " + std::to_string(i + 1) + ")");
+    bound += a / (lengths[i] * lengths[i]);
+  }
+  const double lower = -M_PI * M_PI * bound;
+  if (!(shift > lower))
+    fail("problem: shift " + std::to_string(shift) + " must exceed " + std::to_string(lower) +
+         " for a positive definite operator");
+}
+
+// detail::scale_by_symbol's failure path (poisson.cpp:602-630): the first
+// index in row-major order whose denominator is <= 0, decoded to (k, l).
+void check_symbol(const sfem_plan_s* p) {
+  const int N = p->dim;
+  std::vector<double> mins(N);
+  for (int i = 0; i < N; ++i) {
+    const auto& e = p->tables[i]->host.eig_coeff;
+    mins[i] = p->factors[i] * *std::min_element(e.begin(), e.end());
+  }
+  double total = p->shift;
+  for (int i = 0; i < N; ++i) total += mins[i];
+  if (total > 0) return;
+  std::vector<int> idx(N, 0);
+  double prefix = p->shift;
+  for (int i = 0; i < N; ++i) {
+    double tail = 0;
+    for (int j = i + 1; j < N; ++j) tail += mins[j];
+    const auto& e = p->tables[i]->host.eig_coeff;
+    for (size_t t = 0; t < e.size(); ++t)
+      if (prefix + p->factors[i] * e[t] + tail <= 0 || t + 1 == e.size()) {
+        idx[i] = static_cast<int>(t);
+        prefix += p->factors[i] * e[t];
+        break;
+      }
+  }
+  double denom = p->shift;
+  std::string where;
+  for (int i = 0; i < N; ++i) {
+    denom += p->factors[i] * p->tables[i]->host.eig_coeff[idx[i]];
+    const int n = p->orders[i];
+    int k, l;
+    if (idx[i] < n - 1) {
+      k = 0;
+      l = idx[i] + 1;
+    } else {
+      k = (idx[i] - (n - 1)) / n + 1;
+      l = (idx[i] - (n - 1)) % n + 1;
+    }
+    where += (i ? ", " : "") + std::string("k") + std::to_string(i + 1) + "=" + std::to_string(k) + " l" +
+             std::to_string(i + 1) + "=" + std::to_string(l);
+  }
+  fail("solve: nonpositive denominator " + std::to_string(denom) + " at (" + where + "); shift too negative");
+}
+
+void ensure_work(sfem_plan_s* p) {
+  if (p->dwork) return;
+  ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+  ck(cudaMalloc(&p->dwork, static_cast<size_t>(p->rows) * p->pitch * sizeof(double)), "cudaMalloc(work)");
+}
+
+double event_seconds(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+  return ms * 1e-3;
+}
+
+// ---- class-array (GridFunctionND) <-> dof tensor on the host ----
+// Mapping restated from the reference's oracle::pack_nd / unpack_nd
+// (oracle.cpp:86-144).
+template <bool TO_DOF>
+void classes_dof(const sfem_plan_s* p, const double* const* cls_in, double* const* cls_out, const double* dof_in,
+                 double* dof_out) {
+  const int N = p->dim;
+  std::vector<std::vector<long long>> cidx(N);
+  std::vector<std::vector<unsigned char>> inter(N);
+  for (int i = 0; i < N; ++i) {
+    const int n = p->orders[i];
+    cidx[i].resize(p->ext[i]);
+    inter[i].resize(p->ext[i]);
+    for (long long t = 0; t < p->ext[i]; ++t) {
+      const long long r = t % n;
+      if (r == n - 1) {
+        inter[i][t] = 0;
+        cidx[i][t] = t / n + 1;
+      } else {
+        inter[i][t] = 1;
+        cidx[i][t] = (t / n) * (n - 1) + r;
+      }
+    }
+  }
+  const unsigned ncls = 1u << N;
+  std::vector<std::vector<long long>> cstride(ncls, std::vector<long long>(N));
+  for (unsigned mask = 0; mask < ncls; ++mask) {
+    long long s = 1;
+    for (int i = N - 1; i >= 0; --i) {
+      cstride[mask][i] = s;
+      const long long e = (mask >> i & 1u) ? static_cast<long long>(p->elements[i]) * (p->orders[i] - 1)
+                                           : p->elements[i] + 1;
+      s *= e;
+    }
+  }
+  long long total = 1;
+  for (int i = 0; i < N; ++i) total *= p->ext[i];
+  const long long last = p->ext[N - 1];
+#pragma omp parallel for schedule(static)
+  for (long long row = 0; row < total / last; ++row) {
+    std::vector<long long> idx(N, 0);
+    long long rem = row;
+    for (int i = N - 2; i >= 0; --i) {
+      idx[i] = rem % p->ext[i];
+      rem /= p->ext[i];
+    }
+    for (long long t = 0; t < last; ++t) {
+      idx[N - 1] = t;
+      unsigned mask = 0;
+      for (int i = 0; i < N; ++i)
+        if (inter[i][idx[i]]) mask |= 1u << i;
+      long long off = 0;
+      for (int i = 0; i < N; ++i) off += cidx[i][idx[i]] * cstride[mask][i];
+      if (TO_DOF)
+        dof_out[row * last + t] = cls_in[mask][off];
+      else
+        cls_out[mask][off] = dof_in[row * last + t];
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sfem_cuda_version(void) { return 100; }
+
+const char* sfem_cuda_last_error(void) { return g_err.c_str(); }
+
+int sfem_cuda_ctx_create(int device, sfem_ctx* out) {
+  return guarded([&] {
+    require(out != nullptr, "ctx_create: null output");
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    require(device >= 0 && device < count, "ctx_create: no CUDA device " + std::to_string(device));
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new sfem_ctx_s;
+    c->device = device;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    *out = c;
+  });
+}
+
+int sfem_cuda_ctx_destroy(sfem_ctx ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int sfem_cuda_ctx_stream(sfem_ctx ctx, void** stream) {
+  return guarded([&] {
+    require(ctx && stream, "ctx_stream: null argument");
+    *stream = ctx->stream;
+  });
+}
+
+int sfem_cuda_table_create(sfem_ctx ctx, int order, int elements, sfem_table* out) {
+  return guarded([&] {
+    require(ctx && out, "table_create: null argument");
+    auto t = std::make_unique<sfem_table_s>();
+    t->ctx = ctx;
+    t->host = build_host_table(order, elements);
+    upload_table(t.get());
+    *out = t.release();
+  });
+}
+
+int sfem_cuda_table_destroy(sfem_table t) {
+  return guarded([&] {
+    if (!t) return;
+    if (t->dbuf) cudaFree(t->dbuf);
+    delete t;
+  });
+}
+
+int sfem_cuda_table_export(sfem_table t, double* values, double* norm_sq, double* p, double* interior_values,
+                           double* interior_vectors, double* eig_coeff) {
+  return guarded([&] {
+    require(t != nullptr, "table_export: null table");
+    auto cp = [](const std::vector<double>& v, double* dst) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(t->host.values, values);
+    cp(t->host.norm_sq, norm_sq);
+    cp(t->host.p, p);
+    cp(t->host.interior_values, interior_values);
+    cp(t->host.interior_vectors, interior_vectors);
+    cp(t->host.eig_coeff, eig_coeff);
+  });
+}
+
+int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* d_in, long long in_pitch,
+                           double* d_out, long long out_pitch, void* stream) {
+  return guarded([&] {
+    require(t != nullptr, "lines: null table");
+    require(op >= 0 && op <= 2, "lines: unknown op");
+    require(count >= 0, "lines: negative count");
+    const long long L = t->dev.L;
+    require(in_pitch >= L && out_pitch >= L, "lines: pitch smaller than the line length");
+    if (count == 0) return;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->ctx->stream;
+    ck(cudaSetDevice(t->ctx->device), "cudaSetDevice");
+    const double* src = d_in;
+    if (in_pitch != out_pitch) {
+      ck(cudaMemcpy2DAsync(d_out, out_pitch * sizeof(double), d_in, in_pitch * sizeof(double), L * sizeof(double),
+                           count, cudaMemcpyDeviceToDevice, s),
+         "lines: repitch");
+      src = d_out;
+    }
+    LineSet ls{};
+    ls.src = src;
+    ls.dst = d_out;
+    ls.nlines = count;
+    ls.ninner = 1;
+    ls.n1 = count;
+    ls.is = 0;
+    ls.os1 = out_pitch;
+    ls.os2 = 0;
+    ls.ps = 1;
+    ls.contiguous = 1;
+    const int B = choose_tile(t->dev, count);
+    const int mode = op == SFEM_OP_SYNTHESIZE ? kInverse : kForward;
+    const int analysis = op == SFEM_OP_DECOMPOSE ? kDirect : kWeighted;
+    ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s), "lines launch");
+  });
+}
+
+int sfem_cuda_lines_host(sfem_table t, int op, long long count, const double* h_in, double* h_out) {
+  return guarded([&] {
+    require(t != nullptr, "lines: null table");
+    const long long L = t->dev.L;
+    if (count == 0) return;
+    ck(cudaSetDevice(t->ctx->device), "cudaSetDevice");
+    cudaStream_t s = t->ctx->stream;
+    double* d = nullptr;
+    const size_t bytes = static_cast<size_t>(count) * L * sizeof(double);
+    ck(cudaMallocAsync(&d, bytes, s), "cudaMallocAsync");
+    ck(cudaMemcpyAsync(d, h_in, bytes, cudaMemcpyHostToDevice, s), "H2D");
+    if (sfem_cuda_lines_device(t, op, count, d, L, d, L, s) != 0) {
+      cudaFreeAsync(d, s);
+      throw std::runtime_error(g_err);
+    }
+    ck(cudaMemcpyAsync(h_out, d, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaFreeAsync(d, s), "cudaFreeAsync");
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int sfem_cuda_plan_create(sfem_ctx ctx, int dim, const int* orders, const int* elements, const double* lengths,
+                          const double* coefficients, double shift, sfem_plan* out) {
+  return guarded([&] {
+    require(ctx && orders && elements && lengths && out, "plan_create: null argument");
+    validate(dim, orders, elements, lengths, coefficients, shift);
+    auto p = std::make_unique<sfem_plan_s>();
+    p->ctx = ctx;
+    p->dim = dim;
+    p->orders.assign(orders, orders + dim);
+    p->elements.assign(elements, elements + dim);
+    p->lengths.assign(lengths, lengths + dim);
+    p->coeffs.assign(dim, 1.0);
+    if (coefficients) p->coeffs.assign(coefficients, coefficients + dim);
+    p->shift = shift;
+    std::map<std::pair<int, int>, sfem_table_s*> cache;
+    for (int i = 0; i < dim; ++i) {
+      const auto key = std::make_pair(orders[i], elements[i]);
+      auto it = cache.find(key);
+      if (it == cache.end()) {
+        auto t = std::make_unique<sfem_table_s>();
+        t->ctx = ctx;
+        t->host = build_host_table(orders[i], elements[i]);
+        upload_table(t.get());
+        it = cache.emplace(key, t.get()).first;
+        p->owned.push_back(std::move(t));
+      }
+      p->tables.push_back(it->second);
+      // f_i = a_i * 4 / h_i^2 (axis_scale_factors, poisson.cpp:398-405)
+      const double h = lengths[i] / elements[i];
+      p->factors.push_back(p->coeffs[i] * (4.0 / (h * h)));
+      p->ext.push_back(static_cast<long long>(orders[i]) * elements[i] - 1);
+    }
+    check_symbol(p.get());
+    p->rows = 1;
+    for (int i = 0; i < dim - 1; ++i) p->rows *= p->ext[i];
+    const long long last = p->ext[dim - 1];
+    p->pitch = (last + 3) & ~3LL;  // 32-byte rows
+    build_steps(p.get(), p->pitch);
+    ck(cudaEventCreate(&p->ev[0]), "event");
+    ck(cudaEventCreate(&p->ev[1]), "event");
+    p->kev.resize(p->steps.size() + 1);
+    for (auto& e : p->kev) ck(cudaEventCreate(&e), "event");
+    *out = p.release();
+  });
+}
+
+int sfem_cuda_plan_destroy(sfem_plan p) {
+  return guarded([&] {
+    if (!p) return;
+    cudaSetDevice(p->ctx->device);
+    if (p->dwork) cudaFree(p->dwork);
+    for (auto& t : p->owned)
+      if (t->dbuf) cudaFree(t->dbuf);
+    for (auto e : p->ev)
+      if (e) cudaEventDestroy(e);
+    for (auto e : p->kev)
+      if (e) cudaEventDestroy(e);
+    delete p;
+  });
+}
+
+int sfem_cuda_plan_shape(sfem_plan p, long long* extents, long long* pitch, long long* unknowns) {
+  return guarded([&] {
+    require(p != nullptr, "plan_shape: null plan");
+    long long u = 1;
+    for (int i = 0; i < p->dim; ++i) {
+      if (extents) extents[i] = p->ext[i];
+      u *= p->ext[i];
+    }
+    const long long last = p->ext[p->dim - 1];
+    if (pitch) *pitch = (last + 3) & ~3LL;
+    if (unknowns) *unknowns = u;
+  });
+}
+
+int sfem_cuda_plan_launches(sfem_plan p, int* launches) {
+  return guarded([&] {
+    require(p && launches, "plan_launches: null argument");
+    *launches = static_cast<int>(p->steps.size());
+  });
+}
+
+int sfem_cuda_solve_device(sfem_plan p, double* d_data, long long pitch, void* stream) {
+  return guarded([&] {
+    require(p && d_data, "solve_device: null argument");
+    require(pitch >= p->ext[p->dim - 1], "solve_device: pitch smaller than the last extent");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->ctx->stream;
+    run_steps(p, d_data, pitch, s, false);
+  });
+}
+
+int sfem_cuda_solve_host(sfem_plan p, const double* h_load, double* h_u, double* seconds) {
+  return guarded([&] {
+    require(p && h_load && h_u, "solve_host: null argument");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    const long long pitch = (p->ext[p->dim - 1] + 3) & ~3LL;
+    if (p->pitch != pitch) {
+      build_steps(p, pitch);
+      p->pitch = pitch;
+    }
+    ensure_work(p);
+    cudaStream_t s = p->ctx->stream;
+    const long long last = p->ext[p->dim - 1];
+    ck(cudaMemcpy2DAsync(p->dwork, pitch * sizeof(double), h_load, last * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyHostToDevice, s),
+       "H2D");
+    ck(cudaEventRecord(p->ev[0], s), "event");
+    run_steps(p, p->dwork, pitch, s, false);
+    ck(cudaEventRecord(p->ev[1], s), "event");
+    ck(cudaMemcpy2DAsync(h_u, last * sizeof(double), p->dwork, pitch * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyDeviceToHost, s),
+       "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (seconds) *seconds = event_seconds(p->ev[0], p->ev[1]);
+  });
+}
+
+int sfem_cuda_solve_classes(sfem_plan p, const double* const* h_load_classes, double* const* h_u_classes,
+                            double* seconds) {
+  return guarded([&] {
+    require(p && h_load_classes && h_u_classes, "solve_classes: null argument");
+    long long total = 1;
+    for (int i = 0; i < p->dim; ++i) total *= p->ext[i];
+    std::vector<double> dof(static_cast<size_t>(total));
+    classes_dof<true>(p, h_load_classes, nullptr, nullptr, dof.data());
+    if (sfem_cuda_solve_host(p, dof.data(), dof.data(), seconds) != 0) throw std::runtime_error(g_err);
+    // boundary slots (and anything not covered by a dof) are zero
+    const unsigned ncls = 1u << p->dim;
+    for (unsigned mask = 0; mask < ncls; ++mask) {
+      long long sz = 1;
+      for (int i = 0; i < p->dim; ++i)
+        sz *= (mask >> i & 1u) ? static_cast<long long>(p->elements[i]) * (p->orders[i] - 1) : p->elements[i] + 1;
+      std::fill(h_u_classes[mask], h_u_classes[mask] + sz, 0.0);
+    }
+    classes_dof<false>(p, nullptr, h_u_classes, dof.data(), nullptr);
+  });
+}
+
+int sfem_cuda_solve_device_timed(sfem_plan p, double* d_data, long long pitch, int reps, double* total_ms,
+                                 double* kernel_ms) {
+  return guarded([&] {
+    require(p && d_data && reps >= 1, "solve_device_timed: bad argument");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = p->ctx->stream;
+    std::vector<double> acc(p->steps.size(), 0.0);
+    double total = 0;
+    for (int r = 0; r < reps; ++r) {
+      run_steps(p, d_data, pitch, s, true);
+      ck(cudaStreamSynchronize(s), "sync");
+      for (size_t i = 0; i < p->steps.size(); ++i) acc[i] += event_seconds(p->kev[i], p->kev[i + 1]) * 1e3;
+      total += event_seconds(p->kev[0], p->kev[p->steps.size()]) * 1e3;
+    }
+    if (total_ms) *total_ms = total / reps;
+    if (kernel_ms)
+      for (size_t i = 0; i < acc.size(); ++i) kernel_ms[i] = acc[i] / reps;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// Device-side parameter blocks shared by the sweep kernels and the host
+// orchestrator (capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace sfem_b200 {
+
+constexpr int kMaxDim = 4;
+constexpr int kMaxPasses = 24;
+
+// One (n, K) spectral table in device memory (see table.hpp / DESIGN.md 3).
+struct DevTable {
+  int n, K, m, half, ne, L;
+  const double* mix_fwd_w;  // (K-1) x n x n, [k-1][l][s]
+  const double* mix_fwd_d;
+  const double* mix_inv;    // (K-1) x n x n, [k-1][s][l]
+  const double* e0_fwd_w;   // m x m, [i][l]
+  const double* e0_fwd_d;
+  const double* e0_inv;
+  const double* eig;        // L, coefficient order
+  const double2* tw;        // N: exp(-2 pi i t/N)
+  const double2* mk;        // N: exp(-i pi k/(2N))
+  const double2* mkh;       // N: 0.5 exp(+i pi k/(2N))
+  const double2* om;        // N: exp(-i pi j/N)
+  int npass;
+  int radix[kMaxPasses];    // Stockham pass radices, product = K
+};
+
+// A set of lines along one axis of a tensor.  Line l (0 <= l < nlines) is
+// split as l = (o2 * n1 + o1) * ninner + i and starts at
+// o2*os2 + o1*os1 + i*is; position p of the line is at start + p*ps.  Tiles
+// are read from `src` and written to `dst` at the same offsets (in place when
+// equal).
+struct LineSet {
+  const double* src;
+  double* dst;
+  long long nlines;
+  long long ninner, n1;
+  long long is, os1, os2, ps;
+  int contiguous;  // ps == 1: lines are rows (tile loads run along the line)
+};
+
+// Symbol data for the fused last-axis kernel: a line's leading coordinates
+// (row-major over the leading axes) give base = shift + sum_i f_i lambda_i[a_i]
+// (poisson.cpp:586-590 order), then denom = base + f_last * lambda_last[p].
+struct SymbolInfo {
+  int nlead;
+  long long lead_ext[kMaxDim];
+  const double* lead_eig[kMaxDim];
+  double lead_f[kMaxDim];
+  double shift;
+  double f_last;
+};
+
+enum SweepMode { kForward = 0, kInverse = 1, kForwardDivideInverse = 2 };
+enum AnalysisKind { kWeighted = 0, kDirect = 1 };
+
+// Shared-memory bytes needed for a tile of B lines of table t.
+size_t sweep_smem_bytes(const DevTable& t, int B);
+
+// Launch one sweep over `lines` with tiles of B lines.
+cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int analysis,
+                         const SymbolInfo* sym, int B, cudaStream_t stream);
+
+}  // namespace sfem_b200

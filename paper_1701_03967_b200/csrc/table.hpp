@@ -1,0 +1,59 @@
+// Host-side spectral table builder (cold path, runs once per (n, K) before any
+// device work).  Re-implements, from the reference's published algorithm, the
+// data the sweeps consume:
+//   element matrices          reference include/sfem/element.hpp:258-295
+//   interior pencil eigenpairs element.hpp:140-198, 313-347 (Cholesky+Jacobi,
+//                              smallmat.hpp:72-214)
+//   theta-equation roots      spectral.hpp:26-193
+//   interior vectors / norms  spectral.hpp:198-277
+//   finalised per-k data      spectral.cpp:21-79
+// and then derives the device-side mix matrices that fold the half-angle
+// twiddles and 1/||s||^2 into one n x n matrix per frequency.
+#pragma once
+
+#include <string>
+#include <vector>
+
+namespace sfem_b200 {
+
+struct HostTable {
+  int order = 0, elements = 0;  // n, K
+  // element data
+  std::vector<double> stiffness, mass;  // (n+1)^2 row-major
+  std::vector<double> mass_interior;    // m x m
+  // interior eigensystem (m = n-1)
+  std::vector<double> interior_values;   // m
+  std::vector<double> interior_vectors;  // m x m row-major, column l-1 = e^(l)
+  // per frequency k = 1..K-1, l = 1..n, index (k-1)*n + (l-1)
+  std::vector<double> theta, half_cos, half_sin;  // K-1
+  std::vector<double> values, norm_sq, nodal_weight;
+  std::vector<double> p, q;  // ((k-1)*n + l-1) * m + i
+  std::vector<double> eig_coeff;  // n*K-1 eigenvalues in coefficient order
+
+  int m() const { return order - 1; }
+  int coeff_count() const { return order * elements - 1; }
+};
+
+// Builds the table; throws std::runtime_error with the reference's messages
+// on failure (bracketing, nonpositive norms, order out of range).
+HostTable build_host_table(int n, int K);
+
+// Device-ready arrays for the sweep kernels (see sweep.cu for their use).
+struct DeviceTableData {
+  int n = 0, K = 0;
+  std::vector<double> mix_fwd_w;   // (K-1) x n(l) x n(s): FC_n analysis
+  std::vector<double> mix_fwd_d;   // (K-1) x n(l) x n(s): F_n analysis
+  std::vector<double> mix_inv;     // (K-1) x n(s) x n(l): synthesis
+  std::vector<double> e0_fwd_w;    // m x m [i][l] = e_i^(l) / K
+  std::vector<double> e0_fwd_d;    // m x m [j][l] = (C~ e^(l))_j / K
+  std::vector<double> e0_inv;      // m x m [i][l] = e_i^(l)
+  std::vector<double> eig;         // n*K-1
+  std::vector<double> tw;          // 2N: exp(-2 pi i t/N)   (re, im interleaved)
+  std::vector<double> mk;          // 2N: exp(-i pi k/(2N))
+  std::vector<double> mkh;         // 2N: 0.5 exp(+i pi k/(2N))
+  std::vector<double> om;          // 2N: exp(-i pi j/N)
+};
+
+DeviceTableData derive_device_data(const HostTable& t);
+
+}  // namespace sfem_b200
