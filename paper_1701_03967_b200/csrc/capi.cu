@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -81,6 +82,12 @@ std::vector<int> factor_radices(int N) {
 
 constexpr size_t kSmemMax = 227 * 1024;
 
+// SFEM_GENERIC=1 forces the generic shared-memory kernels (tests compare both).
+bool fast_enabled() {
+  const char* e = std::getenv("SFEM_GENERIC");
+  return !(e && e[0] == '1');
+}
+
 }  // namespace
 
 struct sfem_ctx_s {
@@ -101,7 +108,8 @@ void upload_table(sfem_table_s* t) {
   const DeviceTableData d = derive_device_data(t->host);
   std::vector<const std::vector<double>*> parts = {&d.mix_fwd_w, &d.mix_fwd_d, &d.mix_inv, &d.e0_fwd_w,
                                                    &d.e0_fwd_d,  &d.e0_inv,    &d.eig,     &d.tw,
-                                                   &d.mk,        &d.mkh,       &d.om};
+                                                   &d.mk,        &d.mkh,       &d.om,
+                                                   &d.mixT_w,    &d.mixT_d,    &d.mixT_i};
   std::vector<size_t> offs;
   size_t total = 0;
   for (const auto* p : parts) {
@@ -132,6 +140,9 @@ void upload_table(sfem_table_s* t) {
   v.mk = reinterpret_cast<const double2*>(t->dbuf + offs[8]);
   v.mkh = reinterpret_cast<const double2*>(t->dbuf + offs[9]);
   v.om = reinterpret_cast<const double2*>(t->dbuf + offs[10]);
+  v.mixT_w = t->dbuf + offs[11];
+  v.mixT_d = t->dbuf + offs[12];
+  v.mixT_i = t->dbuf + offs[13];
   const std::vector<int> r = factor_radices(d.K);
   require(static_cast<int>(r.size()) <= kMaxPasses, "table: too many FFT passes");
   v.npass = static_cast<int>(r.size());
@@ -178,6 +189,7 @@ struct sfem_plan_s {
   double* dwork = nullptr;
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> kev;
+  bool use_fast = true;
 };
 
 namespace {
@@ -251,9 +263,12 @@ void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t strea
     s.ls.src = data;
     s.ls.dst = data;
     if (events) ck(cudaEventRecord(p->kev[i], stream), "event");
-    ck(launch_sweep(p->tables[s.axis]->dev, s.ls, s.mode, kWeighted, s.mode == kForwardDivideInverse ? &s.sym : nullptr,
-                    s.B, stream),
-       "sweep launch");
+    const DevTable& dt = p->tables[s.axis]->dev;
+    const SymbolInfo* sym = s.mode == kForwardDivideInverse ? &s.sym : nullptr;
+    if (p->use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous))
+      ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
+    else
+      ck(launch_sweep(dt, s.ls, s.mode, kWeighted, sym, s.B, stream), "sweep launch");
   }
   if (events) ck(cudaEventRecord(p->kev[p->steps.size()], stream), "event");
 }
@@ -497,10 +512,14 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
     ls.os2 = 0;
     ls.ps = 1;
     ls.contiguous = 1;
-    const int B = choose_tile(t->dev, count);
     const int mode = op == SFEM_OP_SYNTHESIZE ? kInverse : kForward;
     const int analysis = op == SFEM_OP_DECOMPOSE ? kDirect : kWeighted;
-    ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s), "lines launch");
+    if (fast_enabled() && has_fast_sweep(t->dev.n, t->dev.K, mode, 1)) {
+      ck(launch_sweep_fast(t->dev, ls, mode, analysis, nullptr, s), "lines launch (fast)");
+    } else {
+      const int B = choose_tile(t->dev, count);
+      ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s), "lines launch");
+    }
   });
 }
 
@@ -539,6 +558,7 @@ int sfem_cuda_plan_create(sfem_ctx ctx, int dim, const int* orders, const int* e
     p->coeffs.assign(dim, 1.0);
     if (coefficients) p->coeffs.assign(coefficients, coefficients + dim);
     p->shift = shift;
+    p->use_fast = fast_enabled();
     std::map<std::pair<int, int>, sfem_table_s*> cache;
     for (int i = 0; i < dim; ++i) {
       const auto key = std::make_pair(orders[i], elements[i]);

@@ -19,6 +19,9 @@ struct DevTable {
   const double* e0_fwd_d;
   const double* e0_inv;
   const double* eig;        // L, coefficient order
+  const double* mixT_w;     // n x n x K, [l][s][k] (k-contiguous copies of mix_fwd_w; k = 0 unused)
+  const double* mixT_d;     // same for mix_fwd_d
+  const double* mixT_i;     // n x n x K, [s][l][k] copy of mix_inv
   const double2* tw;        // N: exp(-2 pi i t/N)
   const double2* mk;        // N: exp(-i pi k/(2N))
   const double2* mkh;       // N: 0.5 exp(+i pi k/(2N))
@@ -58,6 +61,12 @@ enum AnalysisKind { kWeighted = 0, kDirect = 1 };
 
 // Shared-memory bytes needed for a tile of B lines of table t.
 size_t sweep_smem_bytes(const DevTable& t, int B);
+
+// Fast path (sweep_fast.cu) for the (n, K) it was compiled for; returns
+// cudaErrorNotSupported when no specialisation exists.
+cudaError_t launch_sweep_fast(const DevTable& t, const LineSet& lines, int mode, int analysis,
+                              const SymbolInfo* sym, cudaStream_t stream);
+bool has_fast_sweep(int n, int K, int mode, int contiguous);
 
 // Launch one sweep over `lines` with tiles of B lines.
 cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int analysis,

@@ -677,6 +677,18 @@ DeviceTableData derive_device_data(const HostTable& t) {
       d.e0_fwd_d[static_cast<size_t>(i) * m + l] = ce / K;
     }
   d.eig = t.eig_coeff;
+  d.mixT_w.assign(nn * K, 0.0);
+  d.mixT_d.assign(nn * K, 0.0);
+  d.mixT_i.assign(nn * K, 0.0);
+  for (int k = 1; k < K; ++k)
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b) {
+        const size_t src = (k - 1) * nn + static_cast<size_t>(a) * n + b;
+        const size_t dst = (static_cast<size_t>(a) * n + b) * K + k;
+        d.mixT_w[dst] = d.mix_fwd_w[src];
+        d.mixT_d[dst] = d.mix_fwd_d[src];
+        d.mixT_i[dst] = d.mix_inv[src];
+      }
   d.tw.resize(2 * N);
   d.mk.resize(2 * N);
   d.mkh.resize(2 * N);

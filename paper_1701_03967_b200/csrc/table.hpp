@@ -48,6 +48,7 @@ struct DeviceTableData {
   std::vector<double> e0_fwd_d;    // m x m [j][l] = (C~ e^(l))_j / K
   std::vector<double> e0_inv;      // m x m [i][l] = e_i^(l)
   std::vector<double> eig;         // n*K-1
+  std::vector<double> mixT_w, mixT_d, mixT_i;  // n x n x K, k-contiguous (see sweep.cuh)
   std::vector<double> tw;          // 2N: exp(-2 pi i t/N)   (re, im interleaved)
   std::vector<double> mk;          // 2N: exp(-i pi k/(2N))
   std::vector<double> mkh;         // 2N: 0.5 exp(+i pi k/(2N))

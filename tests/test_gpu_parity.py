@@ -204,3 +204,37 @@ def test_config1_matches_reference_cpu_solver(sfem):
     u, _ = sfem.solve_dof(spec, f)
     want, _ = reflib.solve(f, [2, 2], [64, 64], [1.0, 1.0], 0.0)
     assert rel_l2(u, want) <= TOL
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 9])
+def test_fast_kernels_match_generic_and_oracle(sfem, n, monkeypatch):
+    # K = 64 runs the register-FFT kernels (sweep_fast.cu); SFEM_GENERIC=1 forces
+    # the shared-memory Stockham kernels (sweep.cu).  Both must meet the oracle.
+    K = 64
+    spec = sfem.ProblemSpec(2, [1.0, 0.7], [K, K], [n, n], 0.25)
+    f = np.random.default_rng(n).uniform(-1, 1, spec.extents())
+    u_fast, _ = sfem.solve_dof(spec, f)
+    monkeypatch.setenv("SFEM_GENERIC", "1")
+    u_gen, _ = sfem.solve_dof(spec, f)
+    t = sfem.SpectralTable(n, K)
+    x = np.random.default_rng(10 + n).standard_normal((13, n * K - 1))
+    gen_lines = [sfem.lines(t, op, x) for op in (0, 1, 2)]
+    monkeypatch.delenv("SFEM_GENERIC")
+    fast_lines = [sfem.lines(t, op, x) for op in (0, 1, 2)]
+    want = O.solve_full_diagonalization(f, [n, n], [K, K], [1.0, 0.7], 0.25)
+    assert rel_l2(u_fast, want) <= TOL
+    assert rel_l2(u_gen, want) <= TOL
+    assert rel_l2(u_fast, u_gen) <= 1e-13
+    ot = O.table(n, K)
+    for a, b_, fn in zip(fast_lines, gen_lines, (O.decompose_weighted, O.decompose, O.synthesize)):
+        assert rel_l2(a, fn(x, ot)) <= TOL
+        assert rel_l2(a, b_) <= 1e-13
+
+
+def test_fast_3d_partial_tiles(sfem):
+    # line counts that are not multiples of the 8-line tile, 3D, mixed orders
+    spec = sfem.ProblemSpec(3, [1.0, 1.0, 2.0], [64, 3, 64], [3, 2, 2], 1.0)
+    f = np.random.default_rng(7).uniform(-1, 1, spec.extents())
+    u, _ = sfem.solve_dof(spec, f)
+    want = O.solve_full_diagonalization(f, [3, 2, 2], [64, 3, 64], [1.0, 1.0, 2.0], 1.0)
+    assert rel_l2(u, want) <= TOL
