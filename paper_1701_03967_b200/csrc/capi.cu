@@ -641,23 +641,17 @@ int sfem_cuda_solve_host(sfem_plan p, const double* h_load, double* h_u, double*
   return guarded([&] {
     require(p && h_load && h_u, "solve_host: null argument");
     ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
-    const long long pitch = (p->ext[p->dim - 1] + 3) & ~3LL;
-    if (p->pitch != pitch) {
-      build_steps(p, pitch);
-      p->pitch = pitch;
-    }
+    // Dense device copy (pitch = extent): host<->device moves are plain 1D copies.
+    const long long last = p->ext[p->dim - 1];
+    const long long pitch = last;
     ensure_work(p);
     cudaStream_t s = p->ctx->stream;
-    const long long last = p->ext[p->dim - 1];
-    ck(cudaMemcpy2DAsync(p->dwork, pitch * sizeof(double), h_load, last * sizeof(double), last * sizeof(double),
-                         p->rows, cudaMemcpyHostToDevice, s),
-       "H2D");
+    const size_t bytes = static_cast<size_t>(p->rows) * last * sizeof(double);
+    ck(cudaMemcpyAsync(p->dwork, h_load, bytes, cudaMemcpyHostToDevice, s), "H2D");
     ck(cudaEventRecord(p->ev[0], s), "event");
     run_steps(p, p->dwork, pitch, s, false);
     ck(cudaEventRecord(p->ev[1], s), "event");
-    ck(cudaMemcpy2DAsync(h_u, last * sizeof(double), p->dwork, pitch * sizeof(double), last * sizeof(double),
-                         p->rows, cudaMemcpyDeviceToHost, s),
-       "D2H");
+    ck(cudaMemcpyAsync(h_u, p->dwork, bytes, cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
     if (seconds) *seconds = event_seconds(p->ev[0], p->ev[1]);
   });
