@@ -11,7 +11,9 @@
 //                                                 shared memory in between
 //   inverse sweeps along axes N-2..0
 // = 2N-1 launches and 2N-1 passes over HBM instead of 2N.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <chrono>
@@ -170,7 +172,37 @@ struct Step {
   LineSet ls;  // src/dst filled at launch
   int B;
   SymbolInfo sym;
+  // TMA description (strided steps): tensor map for the data pointer it was
+  // encoded for, re-encoded when the pointer changes.
+  bool tma = false;
+  TmaGeom geo{};
+  cuuint64_t dims[4] = {1, 1, 1, 1}, strides[3] = {0, 0, 0};
+  const double* map_ptr = nullptr;
+  alignas(64) CUtensorMap map;
 };
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+    require(q == cudaDriverEntryPointSuccess && p != nullptr, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+void encode_map(Step& s, const double* data) {
+  if (s.map_ptr == data) return;
+  const cuuint32_t box[4] = {8u, static_cast<cuuint32_t>(s.geo.boxp), 1u, 1u};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode_fn()(&s.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(data), s.dims,
+                                 s.strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  s.map_ptr = data;
+}
 
 }  // namespace
 
@@ -225,6 +257,31 @@ void build_steps(sfem_plan_s* p, long long pitch) {
     ls.ps = st[a];
     ls.contiguous = 0;
     s.B = choose_tile(p->tables[a]->dev, nl);
+    const DevTable& dt = p->tables[a]->dev;
+    if (p->use_fast && has_tma_sweep(dt.n, dt.K) && (pitch * 8) % 16 == 0) {
+      s.tma = true;
+      long long total_bytes = 8;
+      for (int i = 0; i < N - 1; ++i) total_bytes *= p->ext[i];
+      total_bytes *= pitch;
+      total_bytes = (total_bytes + 15) & ~15LL;
+      s.dims[0] = p->ext[N - 1];
+      s.dims[1] = p->ext[a];
+      s.strides[0] = st[a] * 8;
+      s.strides[1] = s.strides[2] = total_bytes;
+      if (outer.size() >= 1) {
+        s.dims[2] = p->ext[outer.back()];
+        s.strides[1] = st[outer.back()] * 8;
+      }
+      if (outer.size() == 2) {
+        s.dims[3] = p->ext[outer[0]];
+        s.strides[2] = st[outer[0]] * 8;
+      }
+      s.geo.nbox = static_cast<int>((p->ext[a] + 255) / 256);
+      s.geo.boxp = static_cast<int>((p->ext[a] + s.geo.nbox - 1) / s.geo.nbox);
+      s.geo.nblk0 = (p->ext[N - 1] + 7) / 8;
+      s.geo.ext2 = static_cast<long long>(s.dims[2]);
+      s.geo.ntiles = s.geo.nblk0 * static_cast<long long>(s.dims[2]) * static_cast<long long>(s.dims[3]);
+    }
     p->steps.push_back(s);
   };
   for (int a = 0; a < N - 1; ++a) strided(a, kForward);
@@ -259,13 +316,16 @@ void build_steps(sfem_plan_s* p, long long pitch) {
 void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
   if (pitch != p->pitch) build_steps(p, pitch), p->pitch = pitch;
   for (size_t i = 0; i < p->steps.size(); ++i) {
-    Step s = p->steps[i];
+    Step& s = p->steps[i];
     s.ls.src = data;
     s.ls.dst = data;
     if (events) ck(cudaEventRecord(p->kev[i], stream), "event");
     const DevTable& dt = p->tables[s.axis]->dev;
     const SymbolInfo* sym = s.mode == kForwardDivideInverse ? &s.sym : nullptr;
-    if (p->use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous))
+    if (s.tma) {
+      encode_map(s, data);
+      ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
+    } else if (p->use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous))
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
     else
       ck(launch_sweep(dt, s.ls, s.mode, kWeighted, sym, s.B, stream), "sweep launch");
@@ -641,17 +701,21 @@ int sfem_cuda_solve_host(sfem_plan p, const double* h_load, double* h_u, double*
   return guarded([&] {
     require(p && h_load && h_u, "solve_host: null argument");
     ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
-    // Dense device copy (pitch = extent): host<->device moves are plain 1D copies.
+    // Padded device copy (pitch: 32-byte rows, TMA-compatible); the copy
+    // engine does the re-pitching.
     const long long last = p->ext[p->dim - 1];
-    const long long pitch = last;
+    const long long pitch = (last + 3) & ~3LL;
     ensure_work(p);
     cudaStream_t s = p->ctx->stream;
-    const size_t bytes = static_cast<size_t>(p->rows) * last * sizeof(double);
-    ck(cudaMemcpyAsync(p->dwork, h_load, bytes, cudaMemcpyHostToDevice, s), "H2D");
+    ck(cudaMemcpy2DAsync(p->dwork, pitch * sizeof(double), h_load, last * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyHostToDevice, s),
+       "H2D");
     ck(cudaEventRecord(p->ev[0], s), "event");
     run_steps(p, p->dwork, pitch, s, false);
     ck(cudaEventRecord(p->ev[1], s), "event");
-    ck(cudaMemcpyAsync(h_u, p->dwork, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpy2DAsync(h_u, last * sizeof(double), p->dwork, pitch * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyDeviceToHost, s),
+       "D2H");
     ck(cudaStreamSynchronize(s), "sync");
     if (seconds) *seconds = event_seconds(p->ev[0], p->ev[1]);
   });

@@ -57,6 +57,22 @@ struct SymbolInfo {
 };
 
 enum SweepMode { kForward = 0, kInverse = 1, kForwardDivideInverse = 2 };
+
+// Tile decomposition for the TMA strided kernels: the tensor is viewed as 4-D
+// (d0 = last axis, d1 = swept axis, d2/d3 = remaining axes, size 1 if absent);
+// a tile is 8 consecutive d0 indices x all d1 positions at one (d2, d3).
+struct TmaGeom {
+  int nbox, boxp;      // boxes along d1 (boxp positions each, nbox*boxp >= L)
+  long long nblk0;     // ceil(L_d0 / 8)
+  long long ext2;      // extent of d2
+  long long ntiles;    // nblk0 * ext2 * ext3
+};
+
+// Strided sweep through TMA (sweep_fast.cu).  `tmap` is a CUtensorMap (64-byte
+// aligned opaque blob) describing the in-place tensor.
+cudaError_t launch_sweep_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
+                             cudaStream_t stream);
+bool has_tma_sweep(int n, int K);
 enum AnalysisKind { kWeighted = 0, kDirect = 1 };
 
 // Shared-memory bytes needed for a tile of B lines of table t.
