@@ -32,6 +32,7 @@ CONFIGS = {
     # name: (orders, elements, lengths, coefficients, shift, description)
     "c4": ([9, 9, 9], [64, 64, 64], [1.0] * 3, None, 0.0, "3D n=9 K=64 -Laplace u=f (config 4)"),
     "c1": ([2, 2], [64, 64], [1.0, 1.0], None, 0.0, "2D n=2 K=64 -Laplace u=f (config 1)"),
+    "c3": ([9, 9], [1024, 1024], [1.0, 1.0], [1.0, 2.0], 1.0, "2D n=9 K=1024 -(u_xx+2u_yy)+u=f (config 3)"),
     "c5n1": ([1, 1, 1], [1024] * 3, [1.0] * 3, None, 0.5, "3D n=1 K=1024 -Lap u+0.5u=f (config 5)"),
     "c5n2": ([2, 2, 2], [512] * 3, [1.0] * 3, None, 0.5, "3D n=2 K=512 (config 5)"),
     "c5n4": ([4, 4, 4], [256] * 3, [1.0] * 3, None, 0.5, "3D n=4 K=256 (config 5)"),

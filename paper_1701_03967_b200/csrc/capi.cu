@@ -95,6 +95,8 @@ bool fast_enabled() {
 struct sfem_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
+  double* scratch = nullptr;
+  size_t scratch_doubles = 0;
 };
 
 struct sfem_table_s {
@@ -152,8 +154,11 @@ void upload_table(sfem_table_s* t) {
 }
 
 // Largest tile (lines per CTA) that fits shared memory; prefer two CTAs/SM.
-int choose_tile(const DevTable& t, long long nlines) {
+// Lines too long for any shared-memory tile keep one line per CTA in shared
+// memory and move the FFT work buffers to global scratch (*gwork = true).
+int choose_tile(const DevTable& t, long long nlines, bool* gwork = nullptr) {
   const int cands[] = {16, 8, 4, 2, 1};
+  if (gwork) *gwork = false;
   for (int B : cands) {
     if (B > 1 && B > nlines) continue;
     if (sweep_smem_bytes(t, B) <= kSmemMax / 2) return B;
@@ -161,6 +166,10 @@ int choose_tile(const DevTable& t, long long nlines) {
   for (int B : cands) {
     if (B > 1 && B > nlines) continue;
     if (sweep_smem_bytes(t, B) <= kSmemMax) return B;
+  }
+  if (gwork && sweep_smem_bytes(t, 1, true) <= kSmemMax) {
+    *gwork = true;
+    return 1;
   }
   fail("sfem_cuda: line length " + std::to_string(t.L) + " (n=" + std::to_string(t.n) + ", K=" +
        std::to_string(t.K) + ") exceeds the shared-memory tile of this build");
@@ -171,6 +180,7 @@ struct Step {
   int mode;
   LineSet ls;  // src/dst filled at launch
   int B;
+  bool gwork = false;  // FFT work buffers in global scratch (long lines)
   SymbolInfo sym;
   // TMA description (strided steps): tensor map for the data pointer it was
   // encoded for, re-encoded when the pointer changes.
@@ -224,6 +234,21 @@ struct sfem_plan_s {
   bool use_fast = true;
 };
 
+// Per-context scratch for global-work sweeps (grown on demand).
+static double* scratch_for(sfem_ctx ctx, size_t doubles) {
+  if (doubles > ctx->scratch_doubles) {
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->scratch) {
+      ck(cudaStreamSynchronize(ctx->stream), "sync");
+      ck(cudaFree(ctx->scratch), "cudaFree(scratch)");
+    }
+    ctx->scratch = nullptr;
+    ck(cudaMalloc(&ctx->scratch, doubles * sizeof(double)), "cudaMalloc(scratch)");
+    ctx->scratch_doubles = doubles;
+  }
+  return ctx->scratch;
+}
+
 namespace {
 
 void build_steps(sfem_plan_s* p, long long pitch) {
@@ -256,7 +281,7 @@ void build_steps(sfem_plan_s* p, long long pitch) {
     ls.nlines = nl;
     ls.ps = st[a];
     ls.contiguous = 0;
-    s.B = choose_tile(p->tables[a]->dev, nl);
+    s.B = choose_tile(p->tables[a]->dev, nl, &s.gwork);
     const DevTable& dt = p->tables[a]->dev;
     if (p->use_fast && has_tma_sweep(dt.n, dt.K) && (pitch * 8) % 16 == 0) {
       s.tma = true;
@@ -307,7 +332,7 @@ void build_steps(sfem_plan_s* p, long long pitch) {
     }
     sy.shift = p->shift;
     sy.f_last = p->factors[N - 1];
-    s.B = choose_tile(p->tables[N - 1]->dev, ls.nlines);
+    s.B = choose_tile(p->tables[N - 1]->dev, ls.nlines, &s.gwork);
     p->steps.push_back(s);
   }
   for (int a = N - 2; a >= 0; --a) strided(a, kInverse);
@@ -327,8 +352,11 @@ void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t strea
       ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
     } else if (p->use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous))
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
-    else
-      ck(launch_sweep(dt, s.ls, s.mode, kWeighted, sym, s.B, stream), "sweep launch");
+    else {
+      double* gw = nullptr;
+      if (s.gwork) gw = scratch_for(p->ctx, sweep_work_doubles(dt, s.B) * ((s.ls.nlines + s.B - 1) / s.B));
+      ck(launch_sweep(dt, s.ls, s.mode, kWeighted, sym, s.B, stream, gw), "sweep launch");
+    }
   }
   if (events) ck(cudaEventRecord(p->kev[p->steps.size()], stream), "event");
 }
@@ -496,6 +524,7 @@ int sfem_cuda_ctx_destroy(sfem_ctx ctx) {
   return guarded([&] {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -577,8 +606,10 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
     if (fast_enabled() && has_fast_sweep(t->dev.n, t->dev.K, mode, 1)) {
       ck(launch_sweep_fast(t->dev, ls, mode, analysis, nullptr, s), "lines launch (fast)");
     } else {
-      const int B = choose_tile(t->dev, count);
-      ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s), "lines launch");
+      bool gwork = false;
+      const int B = choose_tile(t->dev, count, &gwork);
+      double* gw = gwork ? scratch_for(t->ctx, sweep_work_doubles(t->dev, B) * ((count + B - 1) / B)) : nullptr;
+      ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s, gw), "lines launch");
     }
   });
 }

@@ -287,7 +287,8 @@ __device__ void inverse_post(const Geometry& g, const double2* R, const double* 
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) sweep_kernel(DevTable t, LineSet ls, int analysis, SymbolInfo sym, int B) {
+__global__ void __launch_bounds__(256) sweep_kernel(DevTable t, LineSet ls, int analysis, SymbolInfo sym, int B,
+                                                    double* gwork) {
   extern __shared__ double smem[];
   const Geometry g = geometry(t, B);
   const int L = g.L, N = g.N, n = g.n, m = g.m;
@@ -296,7 +297,10 @@ __global__ void __launch_bounds__(256) sweep_kernel(DevTable t, LineSet ls, int 
   double* base = C0 + static_cast<size_t>(m) * B;  // B doubles: symbol base per line
   long long* off = reinterpret_cast<long long*>(base + B);
   const size_t head = static_cast<size_t>(L) * B + static_cast<size_t>(m) * B + 2 * static_cast<size_t>(B);
-  double2* W0 = reinterpret_cast<double2*>(smem + head + (head & 1));
+  // FFT work buffers: shared memory, or (long lines) a per-CTA slice of a
+  // global scratch array that stays L2-resident
+  double2* W0 = gwork ? reinterpret_cast<double2*>(gwork + static_cast<size_t>(blockIdx.x) * 4 * g.J * N)
+                      : reinterpret_cast<double2*>(smem + head + (head & 1));
   double2* W1 = W0 + static_cast<size_t>(g.J) * N;
 
   const long long l0 = static_cast<long long>(blockIdx.x) * B;
@@ -409,18 +413,23 @@ __global__ void __launch_bounds__(256) sweep_kernel(DevTable t, LineSet ls, int 
 
 }  // namespace
 
-size_t sweep_smem_bytes(const DevTable& t, int B) {
+size_t sweep_work_doubles(const DevTable& t, int B) {
   const int Bh = (B + 1) / 2;
   const int J = B * t.half + ((t.m & 1) ? Bh : 0) + 2 * Bh;
+  return 4 * static_cast<size_t>(J) * t.K;
+}
+
+size_t sweep_smem_bytes(const DevTable& t, int B, bool global_work) {
   size_t doubles = static_cast<size_t>(t.L) * B + static_cast<size_t>(t.m) * B + 2 * static_cast<size_t>(B);
-  doubles += (doubles & 1) + 4 * static_cast<size_t>(J) * t.K;
+  doubles += (doubles & 1);
+  if (!global_work) doubles += sweep_work_doubles(t, B);
   return doubles * sizeof(double);
 }
 
 cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int analysis,
-                         const SymbolInfo* sym, int B, cudaStream_t stream) {
+                         const SymbolInfo* sym, int B, cudaStream_t stream, double* gwork) {
   if (lines.nlines <= 0) return cudaSuccess;
-  const size_t smem = sweep_smem_bytes(t, B);
+  const size_t smem = sweep_smem_bytes(t, B, gwork != nullptr);
   const long long tiles = (lines.nlines + B - 1) / B;
   SymbolInfo s{};
   if (sym) s = *sym;
@@ -429,17 +438,17 @@ cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int 
   switch (mode) {
     case kForward:
       err = cudaFuncSetAttribute(sweep_kernel<kForward>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (err == cudaSuccess) sweep_kernel<kForward><<<grid, 256, smem, stream>>>(t, lines, analysis, s, B);
+      if (err == cudaSuccess) sweep_kernel<kForward><<<grid, 256, smem, stream>>>(t, lines, analysis, s, B, gwork);
       break;
     case kInverse:
       err = cudaFuncSetAttribute(sweep_kernel<kInverse>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (err == cudaSuccess) sweep_kernel<kInverse><<<grid, 256, smem, stream>>>(t, lines, analysis, s, B);
+      if (err == cudaSuccess) sweep_kernel<kInverse><<<grid, 256, smem, stream>>>(t, lines, analysis, s, B, gwork);
       break;
     default:
       err = cudaFuncSetAttribute(sweep_kernel<kForwardDivideInverse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem));
       if (err == cudaSuccess)
-        sweep_kernel<kForwardDivideInverse><<<grid, 256, smem, stream>>>(t, lines, analysis, s, B);
+        sweep_kernel<kForwardDivideInverse><<<grid, 256, smem, stream>>>(t, lines, analysis, s, B, gwork);
       break;
   }
   if (err != cudaSuccess) return err;

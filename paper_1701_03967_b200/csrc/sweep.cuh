@@ -75,8 +75,11 @@ cudaError_t launch_sweep_tma(const DevTable& t, const void* tmap, const TmaGeom&
 bool has_tma_sweep(int n, int K);
 enum AnalysisKind { kWeighted = 0, kDirect = 1 };
 
-// Shared-memory bytes needed for a tile of B lines of table t.
-size_t sweep_smem_bytes(const DevTable& t, int B);
+// Shared-memory bytes needed for a tile of B lines of table t (FFT work
+// buffers excluded when they live in global scratch).
+size_t sweep_smem_bytes(const DevTable& t, int B, bool global_work = false);
+// Doubles of FFT work buffer per tile (global scratch mode: per CTA).
+size_t sweep_work_doubles(const DevTable& t, int B);
 
 // Fast path (sweep_fast.cu) for the (n, K) it was compiled for; returns
 // cudaErrorNotSupported when no specialisation exists.
@@ -86,6 +89,6 @@ bool has_fast_sweep(int n, int K, int mode, int contiguous);
 
 // Launch one sweep over `lines` with tiles of B lines.
 cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int analysis,
-                         const SymbolInfo* sym, int B, cudaStream_t stream);
+                         const SymbolInfo* sym, int B, cudaStream_t stream, double* gwork = nullptr);
 
 }  // namespace sfem_b200

@@ -238,3 +238,59 @@ def test_fast_3d_partial_tiles(sfem):
     u, _ = sfem.solve_dof(spec, f)
     want = O.solve_full_diagonalization(f, [3, 2, 2], [64, 3, 64], [1.0, 1.0, 2.0], 1.0)
     assert rel_l2(u, want) <= TOL
+
+
+@needs_ref
+@pytest.mark.slow
+def test_config2_full_batch_matches_reference(sfem):
+    # C2: 1D, n=4, K=4096, batch of 4096 lines of length 16383, N(0,1) data:
+    # FC_n and F_n analyses vs the reference's lines::*, and the F_n round trip.
+    n, K = 4, 4096
+    t = sfem.SpectralTable(n, K)
+    x = np.random.default_rng(0).standard_normal((4096, n * K - 1))
+    for op, name in ((sfem.DECOMPOSE_WEIGHTED, "decompose_weighted"), (sfem.DECOMPOSE, "decompose")):
+        got = sfem.lines(t, op, x)
+        want = reflib.lines(name, n, K, x)
+        assert rel_l2(got, want) <= TOL, name
+    c = sfem.lines(t, sfem.DECOMPOSE, x)
+    back = sfem.lines(t, sfem.SYNTHESIZE, c)
+    assert rel_l2(back, x) <= TOL
+    assert rel_l2(back, reflib.lines("synthesize", n, K, c)) <= TOL
+
+
+@needs_ref
+@pytest.mark.slow
+def test_config3_full_size_matches_reference(sfem):
+    # C3: 2D, n=9, K=1024, -(u_xx + 2 u_yy) + u = f on the unit square, f = FEM
+    # load of (9 pi^2 + 1) sin(pi x) sin(2 pi y) + 1e-3 U[-1,1]; the reference
+    # runs it as lengths (1, 1/sqrt 2).
+    n, K = 9, 1024
+    load = reflib.fem_load_sines([n, n], [K, K], [1.0, 1.0], 9 * np.pi ** 2 + 1, [1.0, 2.0])
+    load = load + 1e-3 * reflib.uniform(0, load.size).reshape(load.shape)
+    spec = sfem.ProblemSpec(2, [1.0, 1.0], [K, K], [n, n], 1.0, coefficients=[1.0, 2.0])
+    u, _ = sfem.solve_dof(spec, load)
+    want, _ = reflib.solve(load, [n, n], [K, K], [1.0, 2 ** -0.5], 1.0)
+    assert rel_l2(u, want) <= TOL
+
+
+@needs_ref
+@pytest.mark.slow
+@pytest.mark.parametrize("n,K", [(4, 256), (9, 114)])
+def test_config5_full_size_matches_reference(sfem, n, K):
+    # C5: 3D, nK ~ 1024 per axis (~1.07e9 unknowns, 8.6 GB per FP64 array),
+    # -Laplace u + 0.5 u = f, f ~ U[-1,1]
+    spec = sfem.ProblemSpec(3, [1.0] * 3, [K] * 3, [n] * 3, 0.5)
+    f = np.random.default_rng(0).uniform(-1, 1, spec.extents())
+    u, _ = sfem.solve_dof(spec, f)
+    want, _ = reflib.solve(f, [n] * 3, [K] * 3, [1.0] * 3, 0.5)
+    assert rel_l2(u, want) <= TOL
+
+
+@pytest.mark.parametrize("n,K", [(4, 512), (9, 256), (1, 1024), (2, 300)])
+def test_long_lines_match_oracle(sfem, n, K):
+    # long lines (global-scratch FFT work buffers) against the oracle
+    t = sfem.SpectralTable(n, K)
+    ot = O.table(n, K)
+    x = np.random.default_rng(K).standard_normal((3, n * K - 1))
+    for op, fn in ((0, O.decompose_weighted), (1, O.decompose), (2, O.synthesize)):
+        assert rel_l2(sfem.lines(t, op, x), fn(x, ot)) <= TOL
