@@ -1,0 +1,226 @@
+// C++ parity tests through include/sfem_b200.hpp (the reference-shaped API),
+// restating the reference's own test cases (proj/tests/test_eigenbasis.cpp,
+// test_poisson.cpp).  Built and run by tests/test_cpp_api.py (GPU).
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "sfem_b200.hpp"
+
+using namespace sfem_b200;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                            \
+  do {                                                                         \
+    if (cond) {                                                                \
+      ++g_pass;                                                                \
+    } else {                                                                   \
+      ++g_fail;                                                                \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);              \
+    }                                                                          \
+  } while (0)
+#define CHECK_THROWS(expr)                                                     \
+  do {                                                                         \
+    bool thrown = false;                                                       \
+    try {                                                                      \
+      expr;                                                                    \
+    } catch (const Error&) {                                                   \
+      thrown = true;                                                           \
+    }                                                                          \
+    CHECK(thrown);                                                             \
+  } while (0)
+
+static GridFunction1D random_grid(int n, int K, unsigned seed) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  GridFunction1D g = GridFunction1D::zeros(n, K);
+  for (int j = 1; j < K; ++j) g.nodal[j] = u(rng);
+  for (auto& v : g.interior) v = u(rng);
+  return g;
+}
+
+static CoefficientArray1D random_coeffs(int n, int K, unsigned seed) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  CoefficientArray1D c = CoefficientArray1D::zeros(n, K);
+  for (auto& v : c.data) v = u(rng);
+  return c;
+}
+
+static double max_diff(const std::vector<double>& a, const std::vector<double>& b) {
+  double w = 0;
+  for (size_t i = 0; i < a.size(); ++i) w = std::max(w, std::abs(a[i] - b[i]));
+  return w;
+}
+
+// test_eigenbasis.cpp:106-123
+static void roundtrip_identities(TableSet& tables) {
+  for (int n : {1, 2, 3, 5, 9})
+    for (int K : {2, 3, 4, 8, 31, 64}) {
+      const auto& t = tables.get(n, K);
+      const auto c = random_coeffs(n, K, 1000u + n * 64 + K);
+      const auto back = decompose(synthesize(c, t), t);
+      CHECK(max_diff(c.data, back.data) <= 1e-11);
+      const auto g = random_grid(n, K, 2000u + n * 64 + K);
+      const auto gb = synthesize(decompose(g, t), t);
+      CHECK(max_diff(g.nodal, gb.nodal) <= 1e-11);
+      CHECK(max_diff(g.interior, gb.interior) <= 1e-11);
+    }
+}
+
+// test_eigenbasis.cpp:198-205
+static void dimension_mismatches(TableSet& tables) {
+  const auto& t = tables.get(2, 4);
+  const auto g = random_grid(2, 5, 1);
+  CHECK_THROWS(decompose(g, t));
+  CHECK_THROWS(decompose_weighted(g, t));
+  const auto c = random_coeffs(3, 4, 1);
+  CHECK_THROWS(synthesize(c, t));
+}
+
+// Dense Kronecker reference (oracle.cpp:146-184) on the interleaved dof order.
+static std::vector<double> dense_solve_2d(int n, int K, double shift, const std::vector<double>& rhs) {
+  // element matrices for n = 2 on [-1,1] (exact): stiffness / mass
+  const double A[3][3] = {{7.0 / 6, -4.0 / 3, 1.0 / 6}, {-4.0 / 3, 8.0 / 3, -4.0 / 3}, {1.0 / 6, -4.0 / 3, 7.0 / 6}};
+  const double M[3][3] = {{4.0 / 15, 2.0 / 15, -1.0 / 15}, {2.0 / 15, 16.0 / 15, 2.0 / 15}, {-1.0 / 15, 2.0 / 15, 4.0 / 15}};
+  const int L = n * K - 1;
+  auto dof = [&](int e, int loc) {
+    if (loc == 0) return e == 0 ? -1 : e * n - 1;
+    if (loc == n) return e == K - 1 ? -1 : (e + 1) * n - 1;
+    return e * n + loc - 1;
+  };
+  std::vector<double> a1(L * L, 0.0), c1(L * L, 0.0);
+  for (int e = 0; e < K; ++e)
+    for (int i = 0; i <= n; ++i)
+      for (int j = 0; j <= n; ++j) {
+        const int gi = dof(e, i), gj = dof(e, j);
+        if (gi < 0 || gj < 0) continue;
+        a1[gi * L + gj] += A[i][j];
+        c1[gi * L + gj] += M[i][j];
+      }
+  const double f = 4.0 * K * K;  // 4/h^2 on the unit square
+  const int U = L * L;
+  std::vector<double> S(static_cast<size_t>(U) * U, 0.0), x = rhs;
+  for (int i0 = 0; i0 < L; ++i0)
+    for (int i1 = 0; i1 < L; ++i1)
+      for (int j0 = 0; j0 < L; ++j0)
+        for (int j1 = 0; j1 < L; ++j1)
+          S[static_cast<size_t>(i0 * L + i1) * U + (j0 * L + j1)] =
+              f * (a1[i0 * L + j0] * c1[i1 * L + j1] + c1[i0 * L + j0] * a1[i1 * L + j1]) +
+              shift * c1[i0 * L + j0] * c1[i1 * L + j1];
+  // Gaussian elimination (SPD, no pivoting needed)
+  for (int k = 0; k < U; ++k)
+    for (int i = k + 1; i < U; ++i) {
+      const double r = S[static_cast<size_t>(i) * U + k] / S[static_cast<size_t>(k) * U + k];
+      if (r == 0) continue;
+      for (int j = k; j < U; ++j) S[static_cast<size_t>(i) * U + j] -= r * S[static_cast<size_t>(k) * U + j];
+      x[i] -= r * x[k];
+    }
+  for (int i = U - 1; i >= 0; --i) {
+    double s = x[i];
+    for (int j = i + 1; j < U; ++j) s -= S[static_cast<size_t>(i) * U + j] * x[j];
+    x[i] = s / S[static_cast<size_t>(i) * U + i];
+  }
+  return x;
+}
+
+// test_poisson.cpp:151-160 (2D solve vs the dense Kronecker system), through
+// solve_with_load on the reference's GridFunctionND layout.
+static void solve_vs_dense(TableSet& tables) {
+  const int n = 2, K = 4, L = n * K - 1;
+  ProblemSpec spec;
+  spec.dimension = 2;
+  spec.lengths = {1.0, 1.0};
+  spec.elements = {K, K};
+  spec.orders = {n, n};
+  spec.shift = 1.0;
+  std::mt19937 rng(7);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  std::vector<double> rhs(L * L);
+  for (auto& v : rhs) v = u(rng);
+  // dof -> class arrays
+  GridFunctionND load = GridFunctionND::zeros(spec.axis_specs());
+  auto cls = [&](int t, int& interior, int& idx) {
+    const int r = t % n;
+    interior = r != n - 1;
+    idx = interior ? (t / n) * (n - 1) + r : t / n + 1;
+  };
+  for (int t0 = 0; t0 < L; ++t0)
+    for (int t1 = 0; t1 < L; ++t1) {
+      int m0, i0, m1, i1;
+      cls(t0, m0, i0);
+      cls(t1, m1, i1);
+      const unsigned mask = m0 | (m1 << 1);
+      const int e1 = load.class_extents(mask)[1];
+      load.classes[mask][static_cast<size_t>(i0) * e1 + i1] = rhs[t0 * L + t1];
+    }
+  const SolveReport rep = solve_with_load(spec, load, tables);
+  const std::vector<double> want = dense_solve_2d(n, K, spec.shift, rhs);
+  double worst = 0, scale = 0;
+  for (int t0 = 0; t0 < L; ++t0)
+    for (int t1 = 0; t1 < L; ++t1) {
+      int m0, i0, m1, i1;
+      cls(t0, m0, i0);
+      cls(t1, m1, i1);
+      const unsigned mask = m0 | (m1 << 1);
+      const int e1 = rep.solution.class_extents(mask)[1];
+      worst = std::max(worst, std::abs(rep.solution.classes[mask][static_cast<size_t>(i0) * e1 + i1] - want[t0 * L + t1]));
+      scale = std::max(scale, std::abs(want[t0 * L + t1]));
+    }
+  CHECK(worst <= 1e-10 * std::max(1.0, scale));
+  // boundary slots are zero (enforce_boundary)
+  CHECK(rep.solution.classes[0][0] == 0.0);
+  CHECK(rep.seconds_solve >= 0.0);
+}
+
+// test_poisson.cpp:276-291
+static void rejects_invalid(TableSet& tables) {
+  ProblemSpec spec;
+  spec.dimension = 2;
+  spec.lengths = {1.0, 1.0};
+  spec.elements = {4, 4};
+  spec.orders = {2, 2};
+  spec.shift = -2 * M_PI * M_PI - 1;
+  GridFunctionND load = GridFunctionND::zeros(spec.axis_specs());
+  CHECK_THROWS(solve_with_load(spec, load, tables));
+  ProblemSpec bad = spec;
+  bad.shift = 1.0;
+  bad.elements = {4};
+  CHECK_THROWS(bad.validate());
+  ProblemSpec one = spec;
+  one.shift = 1.0;
+  SolveOptions opt;
+  opt.algorithm = Algorithm::PartialDiagonalization;
+  CHECK_THROWS(solve_with_load(one, load, tables, opt));
+}
+
+// test_poisson.cpp:355-362 (bitwise reproducibility)
+static void deterministic(TableSet& tables) {
+  ProblemSpec spec;
+  spec.dimension = 3;
+  spec.lengths = {1.0, 1.0, 1.0};
+  spec.elements = {8, 8, 8};
+  spec.orders = {9, 9, 9};
+  spec.shift = 0.0;
+  Plan plan(tables.context(), spec);
+  const int L = 9 * 8 - 1;
+  std::vector<double> f(static_cast<size_t>(L) * L * L), u1(f.size()), u2(f.size());
+  std::mt19937 rng(3);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  for (auto& v : f) v = u(rng);
+  plan.solve_dof(f.data(), u1.data());
+  plan.solve_dof(f.data(), u2.data());
+  CHECK(max_diff(u1, u2) == 0.0);
+}
+
+int main() {
+  TableSet tables;
+  roundtrip_identities(tables);
+  dimension_mismatches(tables);
+  solve_vs_dense(tables);
+  rejects_invalid(tables);
+  deterministic(tables);
+  std::printf("%d passed, %d failed\n", g_pass, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
