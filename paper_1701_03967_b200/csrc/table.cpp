@@ -685,9 +685,11 @@ DeviceTableData derive_device_data(const HostTable& t) {
       for (int b = 0; b < n; ++b) {
         const size_t src = (k - 1) * nn + static_cast<size_t>(a) * n + b;
         const size_t dst = (static_cast<size_t>(a) * n + b) * K + k;
-        d.mixT_w[dst] = d.mix_fwd_w[src];
-        d.mixT_d[dst] = d.mix_fwd_d[src];
-        d.mixT_i[dst] = d.mix_inv[src];
+        // fast kernels: the 1/2 of the nodal DST-I post-processing lives in the
+        // nodal column (forward, s = 0) / nodal row (inverse, s = 0) of the mix
+        d.mixT_w[dst] = d.mix_fwd_w[src] * (b == 0 ? 0.5 : 1.0);
+        d.mixT_d[dst] = d.mix_fwd_d[src] * (b == 0 ? 0.5 : 1.0);
+        d.mixT_i[dst] = d.mix_inv[src] * (a == 0 ? 0.5 : 1.0);
       }
   d.tw.resize(2 * N);
   d.mk.resize(2 * N);
