@@ -106,6 +106,30 @@ int sfem_cuda_solve_classes(sfem_plan plan, const double* const* h_load_classes,
 int sfem_cuda_solve_device_timed(sfem_plan plan, double* d_data, long long pitch, int reps, double* total_ms,
                                  double* kernel_ms);
 
+/* ---- Multi-GPU slab decomposition (one process / context per GPU) ----
+ * Rank r owns the x-slab of axis-0 dof rows [x0, x0+lx) of the global dof
+ * tensor (all other axes; last axis padded to xpitch) and, between the two
+ * all-to-all exchanges, the y-slab of axis-1 rows [y0, y0+ly) stored as
+ * [ly][R][ypitch] with axis 0 contiguous (R = prod of the extents of axes
+ * 2..N-1).  One solve = FORWARD_LOCAL(x), PACK1(x->buf), all-to-all(buf),
+ * UNPACK1(buf->y), AXIS0(y), PACK2(y->buf), all-to-all(buf, reverse counts),
+ * UNPACK2(buf->x), INVERSE_LOCAL(x).  The exchanges are the caller's (NCCL,
+ * e.g. torch.distributed.all_to_all_single); split sizes from dist_shape.
+ * Replaces the same run_full_diagonalization (poisson.cpp:637-669), sharded. */
+typedef struct sfem_dist_s* sfem_dist;
+enum {
+  SFEM_DIST_FORWARD_LOCAL = 0, SFEM_DIST_PACK1 = 1, SFEM_DIST_UNPACK1 = 2, SFEM_DIST_AXIS0 = 3,
+  SFEM_DIST_PACK2 = 4, SFEM_DIST_UNPACK2 = 5, SFEM_DIST_INVERSE_LOCAL = 6
+};
+int sfem_cuda_dist_create(sfem_ctx ctx, int dim, const int* orders, const int* elements, const double* lengths,
+                          const double* coefficients, double shift, int nranks, int rank, sfem_dist* out);
+int sfem_cuda_dist_destroy(sfem_dist dist);
+/* info[10] = {x0, lx, y0, ly, x-slab elements, y-slab elements, exchange
+ * buffer elements, xpitch, ypitch, R}; send/recv_counts[nranks] (elements) of
+ * exchange 1 (exchange 2 swaps them); either may be NULL. */
+int sfem_cuda_dist_shape(sfem_dist dist, long long* info, long long* send_counts, long long* recv_counts);
+int sfem_cuda_dist_phase(sfem_dist dist, int phase, double* d_x, double* d_y, double* d_buf, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

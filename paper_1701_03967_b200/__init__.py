@@ -78,6 +78,11 @@ _SIGS = [
     ("sfem_cuda_solve_classes", ctypes.c_int, [_vp, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _dp]),
     ("sfem_cuda_solve_device_timed", ctypes.c_int,
      [_vp, _vp, ctypes.c_longlong, ctypes.c_int, _dp, _dp]),
+    ("sfem_cuda_dist_create", ctypes.c_int,
+     [_vp, ctypes.c_int, _ip, _ip, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_dist_destroy", ctypes.c_int, [_vp]),
+    ("sfem_cuda_dist_shape", ctypes.c_int, [_vp, _llp, _llp, _llp]),
+    ("sfem_cuda_dist_phase", ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, _vp]),
 ]
 HEADER_SYMBOLS = [s[0] for s in _SIGS]
 for _name, _res, _args in _SIGS:

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/sfem_cuda.h"
+#include "dist.cuh"
 #include "sweep.cuh"
 #include "table.hpp"
 
@@ -178,6 +179,8 @@ int choose_tile(const DevTable& t, long long nlines, bool* gwork = nullptr) {
 struct Step {
   int axis;
   int mode;
+  sfem_table_s* table = nullptr;  // table of the swept axis
+  bool use_fast = true;
   LineSet ls;  // src/dst filled at launch
   int B;
   bool gwork = false;  // FFT work buffers in global scratch (long lines)
@@ -216,6 +219,161 @@ void encode_map(Step& s, const double* data) {
 
 }  // namespace
 
+// Per-context scratch for global-work sweeps (grown on demand).
+static double* scratch_for(sfem_ctx ctx, size_t doubles) {
+  if (doubles > ctx->scratch_doubles) {
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->scratch) {
+      ck(cudaStreamSynchronize(ctx->stream), "sync");
+      ck(cudaFree(ctx->scratch), "cudaFree(scratch)");
+    }
+    ctx->scratch = nullptr;
+    ck(cudaMalloc(&ctx->scratch, doubles * sizeof(double)), "cudaMalloc(scratch)");
+    ctx->scratch_doubles = doubles;
+  }
+  return ctx->scratch;
+}
+
+namespace {
+
+// A local dof tensor the steps run on: extents (last axis padded to pitch),
+// the table / symbol factor of each of its axes (eig_off shifts an axis's
+// eigenvalue array for slabs that start at a global offset).
+struct View {
+  int N = 0;
+  std::vector<long long> ext;
+  long long pitch = 0;
+  std::vector<sfem_table_s*> tables;
+  std::vector<double> factors;
+  std::vector<long long> eig_off;
+  double shift = 0;
+  bool use_fast = true;
+  long long rows() const {
+    long long r = 1;
+    for (int i = 0; i < N - 1; ++i) r *= ext[i];
+    return r;
+  }
+  std::vector<long long> strides() const {
+    std::vector<long long> st(N);
+    st[N - 1] = 1;
+    if (N >= 2) st[N - 2] = pitch;
+    for (int i = N - 3; i >= 0; --i) st[i] = st[i + 1] * ext[i + 1];
+    return st;
+  }
+};
+
+// Sweep along strided axis a (a < N-1) of view v.
+Step strided_step(const View& v, int a, int mode) {
+  const int N = v.N;
+  const std::vector<long long> st = v.strides();
+  Step s{};
+  s.axis = a;
+  s.mode = mode;
+  s.table = v.tables[a];
+  s.use_fast = v.use_fast;
+  LineSet& ls = s.ls;
+  ls.ninner = v.ext[N - 1];
+  ls.is = 1;
+  std::vector<int> outer;
+  for (int i = 0; i < N - 1; ++i)
+    if (i != a) outer.push_back(i);
+  ls.n1 = 1;
+  ls.os1 = 0;
+  ls.os2 = 0;
+  if (outer.size() >= 1) {
+    ls.n1 = v.ext[outer.back()];
+    ls.os1 = st[outer.back()];
+  }
+  if (outer.size() == 2) ls.os2 = st[outer[0]];
+  long long nl = ls.ninner;
+  for (int i : outer) nl *= v.ext[i];
+  ls.nlines = nl;
+  ls.ps = st[a];
+  ls.contiguous = 0;
+  s.B = choose_tile(v.tables[a]->dev, nl, &s.gwork);
+  const DevTable& dt = v.tables[a]->dev;
+  if (v.use_fast && has_tma_sweep(dt.n, dt.K) && (v.pitch * 8) % 16 == 0) {
+    s.tma = true;
+    long long total_bytes = 8 * v.rows() * v.pitch;
+    total_bytes = (total_bytes + 15) & ~15LL;
+    s.dims[0] = v.ext[N - 1];
+    s.dims[1] = v.ext[a];
+    s.strides[0] = st[a] * 8;
+    s.strides[1] = s.strides[2] = total_bytes;
+    if (outer.size() >= 1) {
+      s.dims[2] = v.ext[outer.back()];
+      s.strides[1] = st[outer.back()] * 8;
+    }
+    if (outer.size() == 2) {
+      s.dims[3] = v.ext[outer[0]];
+      s.strides[2] = st[outer[0]] * 8;
+    }
+    s.geo.nbox = static_cast<int>((v.ext[a] + 255) / 256);
+    s.geo.boxp = static_cast<int>((v.ext[a] + s.geo.nbox - 1) / s.geo.nbox);
+    s.geo.nblk0 = (v.ext[N - 1] + 7) / 8;
+    s.geo.ext2 = static_cast<long long>(s.dims[2]);
+    s.geo.ntiles = s.geo.nblk0 * static_cast<long long>(s.dims[2]) * static_cast<long long>(s.dims[3]);
+  }
+  return s;
+}
+
+// Sweep along the last (contiguous) axis; mode kForwardDivideInverse fuses the
+// symbol divide with the view's leading axes as the symbol's leading terms.
+Step rows_step(const View& v, int mode) {
+  const int N = v.N;
+  Step s{};
+  s.axis = N - 1;
+  s.mode = mode;
+  s.table = v.tables[N - 1];
+  s.use_fast = v.use_fast;
+  LineSet& ls = s.ls;
+  ls.nlines = v.rows();
+  ls.ninner = 1;
+  ls.n1 = ls.nlines;
+  ls.is = 0;
+  ls.os1 = v.pitch;
+  ls.os2 = 0;
+  ls.ps = 1;
+  ls.contiguous = 1;
+  SymbolInfo& sy = s.sym;
+  sy.nlead = N - 1;
+  for (int i = 0; i < N - 1; ++i) {
+    sy.lead_ext[i] = v.ext[i];
+    sy.lead_eig[i] = v.tables[i]->dev.eig + v.eig_off[i];
+    sy.lead_f[i] = v.factors[i];
+  }
+  sy.shift = v.shift;
+  sy.f_last = v.factors[N - 1];
+  s.B = choose_tile(v.tables[N - 1]->dev, ls.nlines, &s.gwork);
+  return s;
+}
+
+// Launch a list of steps on `data` (in place).
+void launch_steps(std::vector<Step>& steps, double* data, sfem_ctx ctx, cudaStream_t stream,
+                  std::vector<cudaEvent_t>* kev) {
+  for (size_t i = 0; i < steps.size(); ++i) {
+    Step& s = steps[i];
+    s.ls.src = data;
+    s.ls.dst = data;
+    if (kev) ck(cudaEventRecord((*kev)[i], stream), "event");
+    const DevTable& dt = s.table->dev;
+    const SymbolInfo* sym = s.mode == kForwardDivideInverse ? &s.sym : nullptr;
+    if (s.tma) {
+      encode_map(s, data);
+      ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
+    } else if (s.use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous)) {
+      ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
+    } else {
+      double* gw = nullptr;
+      if (s.gwork) gw = scratch_for(ctx, sweep_work_doubles(dt, s.B) * ((s.ls.nlines + s.B - 1) / s.B));
+      ck(launch_sweep(dt, s.ls, s.mode, kWeighted, sym, s.B, stream, gw), "sweep launch");
+    }
+  }
+  if (kev) ck(cudaEventRecord((*kev)[steps.size()], stream), "event");
+}
+
+}  // namespace
+
 struct sfem_plan_s {
   sfem_ctx ctx = nullptr;
   int dim = 0;
@@ -234,131 +392,33 @@ struct sfem_plan_s {
   bool use_fast = true;
 };
 
-// Per-context scratch for global-work sweeps (grown on demand).
-static double* scratch_for(sfem_ctx ctx, size_t doubles) {
-  if (doubles > ctx->scratch_doubles) {
-    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    if (ctx->scratch) {
-      ck(cudaStreamSynchronize(ctx->stream), "sync");
-      ck(cudaFree(ctx->scratch), "cudaFree(scratch)");
-    }
-    ctx->scratch = nullptr;
-    ck(cudaMalloc(&ctx->scratch, doubles * sizeof(double)), "cudaMalloc(scratch)");
-    ctx->scratch_doubles = doubles;
-  }
-  return ctx->scratch;
-}
-
 namespace {
+
+View plan_view(const sfem_plan_s* p, long long pitch) {
+  View v;
+  v.N = p->dim;
+  v.ext = p->ext;
+  v.pitch = pitch;
+  v.tables = p->tables;
+  v.factors = p->factors;
+  v.eig_off.assign(p->dim, 0);
+  v.shift = p->shift;
+  v.use_fast = p->use_fast;
+  return v;
+}
 
 void build_steps(sfem_plan_s* p, long long pitch) {
   const int N = p->dim;
-  std::vector<long long> st(N);
-  st[N - 1] = 1;
-  if (N >= 2) st[N - 2] = pitch;
-  for (int i = N - 3; i >= 0; --i) st[i] = st[i + 1] * p->ext[i + 1];
+  const View v = plan_view(p, pitch);
   p->steps.clear();
-  auto strided = [&](int a, int mode) {
-    Step s{};
-    s.axis = a;
-    s.mode = mode;
-    LineSet& ls = s.ls;
-    ls.ninner = p->ext[N - 1];
-    ls.is = 1;
-    std::vector<int> outer;
-    for (int i = 0; i < N - 1; ++i)
-      if (i != a) outer.push_back(i);
-    ls.n1 = 1;
-    ls.os1 = 0;
-    ls.os2 = 0;
-    if (outer.size() >= 1) {
-      ls.n1 = p->ext[outer.back()];
-      ls.os1 = st[outer.back()];
-    }
-    if (outer.size() == 2) ls.os2 = st[outer[0]];
-    long long nl = ls.ninner;
-    for (int i : outer) nl *= p->ext[i];
-    ls.nlines = nl;
-    ls.ps = st[a];
-    ls.contiguous = 0;
-    s.B = choose_tile(p->tables[a]->dev, nl, &s.gwork);
-    const DevTable& dt = p->tables[a]->dev;
-    if (p->use_fast && has_tma_sweep(dt.n, dt.K) && (pitch * 8) % 16 == 0) {
-      s.tma = true;
-      long long total_bytes = 8;
-      for (int i = 0; i < N - 1; ++i) total_bytes *= p->ext[i];
-      total_bytes *= pitch;
-      total_bytes = (total_bytes + 15) & ~15LL;
-      s.dims[0] = p->ext[N - 1];
-      s.dims[1] = p->ext[a];
-      s.strides[0] = st[a] * 8;
-      s.strides[1] = s.strides[2] = total_bytes;
-      if (outer.size() >= 1) {
-        s.dims[2] = p->ext[outer.back()];
-        s.strides[1] = st[outer.back()] * 8;
-      }
-      if (outer.size() == 2) {
-        s.dims[3] = p->ext[outer[0]];
-        s.strides[2] = st[outer[0]] * 8;
-      }
-      s.geo.nbox = static_cast<int>((p->ext[a] + 255) / 256);
-      s.geo.boxp = static_cast<int>((p->ext[a] + s.geo.nbox - 1) / s.geo.nbox);
-      s.geo.nblk0 = (p->ext[N - 1] + 7) / 8;
-      s.geo.ext2 = static_cast<long long>(s.dims[2]);
-      s.geo.ntiles = s.geo.nblk0 * static_cast<long long>(s.dims[2]) * static_cast<long long>(s.dims[3]);
-    }
-    p->steps.push_back(s);
-  };
-  for (int a = 0; a < N - 1; ++a) strided(a, kForward);
-  {
-    Step s{};
-    s.axis = N - 1;
-    s.mode = kForwardDivideInverse;
-    LineSet& ls = s.ls;
-    ls.nlines = p->rows;
-    ls.ninner = 1;
-    ls.n1 = p->rows;
-    ls.is = 0;
-    ls.os1 = pitch;
-    ls.os2 = 0;
-    ls.ps = 1;
-    ls.contiguous = 1;
-    SymbolInfo& sy = s.sym;
-    sy.nlead = N - 1;
-    for (int i = 0; i < N - 1; ++i) {
-      sy.lead_ext[i] = p->ext[i];
-      sy.lead_eig[i] = p->tables[i]->dev.eig;
-      sy.lead_f[i] = p->factors[i];
-    }
-    sy.shift = p->shift;
-    sy.f_last = p->factors[N - 1];
-    s.B = choose_tile(p->tables[N - 1]->dev, ls.nlines, &s.gwork);
-    p->steps.push_back(s);
-  }
-  for (int a = N - 2; a >= 0; --a) strided(a, kInverse);
+  for (int a = 0; a < N - 1; ++a) p->steps.push_back(strided_step(v, a, kForward));
+  p->steps.push_back(rows_step(v, kForwardDivideInverse));
+  for (int a = N - 2; a >= 0; --a) p->steps.push_back(strided_step(v, a, kInverse));
 }
 
 void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
   if (pitch != p->pitch) build_steps(p, pitch), p->pitch = pitch;
-  for (size_t i = 0; i < p->steps.size(); ++i) {
-    Step& s = p->steps[i];
-    s.ls.src = data;
-    s.ls.dst = data;
-    if (events) ck(cudaEventRecord(p->kev[i], stream), "event");
-    const DevTable& dt = p->tables[s.axis]->dev;
-    const SymbolInfo* sym = s.mode == kForwardDivideInverse ? &s.sym : nullptr;
-    if (s.tma) {
-      encode_map(s, data);
-      ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
-    } else if (p->use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous))
-      ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
-    else {
-      double* gw = nullptr;
-      if (s.gwork) gw = scratch_for(p->ctx, sweep_work_doubles(dt, s.B) * ((s.ls.nlines + s.B - 1) / s.B));
-      ck(launch_sweep(dt, s.ls, s.mode, kWeighted, sym, s.B, stream, gw), "sweep launch");
-    }
-  }
-  if (events) ck(cudaEventRecord(p->kev[p->steps.size()], stream), "event");
+  launch_steps(p->steps, data, p->ctx, stream, events ? &p->kev : nullptr);
 }
 
 // Reference ProblemSpec::validate (poisson.cpp:32-47), with per-axis coefficients.
@@ -496,6 +556,43 @@ void classes_dof(const sfem_plan_s* p, const double* const* cls_in, double* cons
         cls_out[mask][off] = dof_in[row * last + t];
     }
   }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Multi-GPU slab plan.  Rank r holds the x-slab of axis-0 rows
+// [x0_r, x0_r + lx_r) (all other axes; last axis padded) and, between the two
+// exchanges, the y-slab of axis-1 rows [y0_r, y0_r + ly_r) stored as
+// [ly][R][P0] with axis 0 contiguous (R = prod of the extents of axes 2..N-1).
+// ---------------------------------------------------------------------------
+struct sfem_dist_s {
+  sfem_ctx ctx = nullptr;
+  int dim = 0, nranks = 1, rank = 0;
+  std::vector<std::unique_ptr<sfem_table_s>> owned;
+  std::vector<sfem_table_s*> tables;
+  std::vector<long long> ext;
+  std::vector<double> factors;
+  double shift = 0;
+  std::vector<long long> x0, lx, y0, ly;
+  long long R = 1, xpitch = 0, ypitch = 0;
+  View xv, yv;
+  std::vector<Step> phaseA, phaseB, phaseC;
+  SlabView sv{};
+};
+
+namespace {
+
+std::vector<long long> balanced(long long n, int parts, std::vector<long long>& off) {
+  std::vector<long long> len(parts);
+  off.assign(parts, 0);
+  long long acc = 0;
+  for (int r = 0; r < parts; ++r) {
+    len[r] = n / parts + (r < n % parts ? 1 : 0);
+    off[r] = acc;
+    acc += len[r];
+  }
+  return len;
 }
 
 }  // namespace
@@ -790,6 +887,183 @@ int sfem_cuda_solve_device_timed(sfem_plan p, double* d_data, long long pitch, i
     if (total_ms) *total_ms = total / reps;
     if (kernel_ms)
       for (size_t i = 0; i < acc.size(); ++i) kernel_ms[i] = acc[i] / reps;
+  });
+}
+
+
+int sfem_cuda_dist_create(sfem_ctx ctx, int dim, const int* orders, const int* elements, const double* lengths,
+                          const double* coefficients, double shift, int nranks, int rank, sfem_dist* out) {
+  return guarded([&] {
+    require(ctx && orders && elements && lengths && out, "dist_create: null argument");
+    require(dim >= 2, "dist_create: the slab decomposition needs dimension >= 2");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "dist_create: bad rank / nranks");
+    validate(dim, orders, elements, lengths, coefficients, shift);
+    auto d = std::make_unique<sfem_dist_s>();
+    d->ctx = ctx;
+    d->dim = dim;
+    d->nranks = nranks;
+    d->rank = rank;
+    d->shift = shift;
+    std::map<std::pair<int, int>, sfem_table_s*> cache;
+    for (int i = 0; i < dim; ++i) {
+      const auto key = std::make_pair(orders[i], elements[i]);
+      auto it = cache.find(key);
+      if (it == cache.end()) {
+        auto t = std::make_unique<sfem_table_s>();
+        t->ctx = ctx;
+        t->host = build_host_table(orders[i], elements[i]);
+        upload_table(t.get());
+        it = cache.emplace(key, t.get()).first;
+        d->owned.push_back(std::move(t));
+      }
+      d->tables.push_back(it->second);
+      const double h = lengths[i] / elements[i];
+      d->factors.push_back((coefficients ? coefficients[i] : 1.0) * (4.0 / (h * h)));
+      d->ext.push_back(static_cast<long long>(orders[i]) * elements[i] - 1);
+    }
+    require(d->ext[0] >= nranks && d->ext[1] >= nranks, "dist_create: fewer slab rows than ranks");
+    d->lx = balanced(d->ext[0], nranks, d->x0);
+    d->ly = balanced(d->ext[1], nranks, d->y0);
+    for (int i = 2; i < dim; ++i) d->R *= d->ext[i];
+    d->xpitch = (d->ext[dim - 1] + 3) & ~3LL;
+    d->ypitch = (d->ext[0] + 3) & ~3LL;
+    const bool fast = fast_enabled();
+    // x view: [lx][L1]..[L_{N-1}]
+    View& xv = d->xv;
+    xv.N = dim;
+    xv.ext = d->ext;
+    xv.ext[0] = d->lx[rank];
+    xv.pitch = d->xpitch;
+    xv.tables = d->tables;
+    xv.factors = d->factors;
+    xv.eig_off.assign(dim, 0);
+    xv.shift = shift;
+    xv.use_fast = fast;
+    // y view: [ly][L2]..[L_{N-1}][L0] (axis 0 last, contiguous)
+    View& yv = d->yv;
+    yv.N = dim;
+    yv.ext.clear();
+    yv.tables.clear();
+    yv.factors.clear();
+    yv.eig_off.clear();
+    for (int i = 1; i < dim; ++i) {
+      yv.ext.push_back(i == 1 ? d->ly[rank] : d->ext[i]);
+      yv.tables.push_back(d->tables[i]);
+      yv.factors.push_back(d->factors[i]);
+      yv.eig_off.push_back(i == 1 ? d->y0[rank] : 0);
+    }
+    yv.ext.push_back(d->ext[0]);
+    yv.tables.push_back(d->tables[0]);
+    yv.factors.push_back(d->factors[0]);
+    yv.eig_off.push_back(0);
+    yv.pitch = d->ypitch;
+    yv.shift = shift;
+    yv.use_fast = fast;
+    // phase A: forward along axes N-1 (rows) and N-2..1 (strided) on the x-slab
+    if (xv.ext[0] > 0) {
+      d->phaseA.push_back(rows_step(xv, kForward));
+      for (int a = dim - 2; a >= 1; --a) d->phaseA.push_back(strided_step(xv, a, kForward));
+      for (int a = 1; a <= dim - 2; ++a) d->phaseC.push_back(strided_step(xv, a, kInverse));
+      d->phaseC.push_back(rows_step(xv, kInverse));
+    }
+    // phase B: fused forward + divide + inverse along axis 0 on the y-slab
+    if (yv.ext[0] > 0) d->phaseB.push_back(rows_step(yv, kForwardDivideInverse));
+    // transpose view of the x-slab
+    const std::vector<long long> st = xv.strides();
+    SlabView& sv = d->sv;
+    sv.lx = d->lx[rank];
+    sv.R = d->R;
+    sv.Q = d->ext[1] * d->R;
+    sv.st0 = st[0];
+    sv.st1 = st[1];
+    sv.nrest = dim - 2;
+    sv.st2 = dim >= 4 ? st[2] : 0;
+    sv.e3 = dim >= 4 ? d->ext[3] : 1;
+    require(dim <= 4, "dist_create: dimension above 4 is not supported by this build");
+    *out = d.release();
+  });
+}
+
+int sfem_cuda_dist_destroy(sfem_dist d) {
+  return guarded([&] {
+    if (!d) return;
+    cudaSetDevice(d->ctx->device);
+    for (auto& t : d->owned)
+      if (t->dbuf) cudaFree(t->dbuf);
+    delete d;
+  });
+}
+
+int sfem_cuda_dist_shape(sfem_dist d, long long* info, long long* send_counts, long long* recv_counts) {
+  return guarded([&] {
+    require(d && info, "dist_shape: null argument");
+    const int r = d->rank;
+    info[0] = d->x0[r];
+    info[1] = d->lx[r];
+    info[2] = d->y0[r];
+    info[3] = d->ly[r];
+    info[4] = d->xv.rows() * d->xpitch;  // x-slab elements (padded)
+    info[5] = d->ly[r] * d->R * d->ypitch;  // y-slab elements
+    long long sx = 0, rx = 0;
+    for (int p = 0; p < d->nranks; ++p) {
+      const long long sc = d->lx[r] * d->ly[p] * d->R;  // exchange 1: to p
+      const long long rc = d->lx[p] * d->ly[r] * d->R;  // exchange 1: from p
+      if (send_counts) send_counts[p] = sc;
+      if (recv_counts) recv_counts[p] = rc;
+      sx += sc;
+      rx += rc;
+    }
+    info[6] = std::max(sx, rx);  // exchange buffer elements (each direction)
+    info[7] = d->xpitch;
+    info[8] = d->ypitch;
+    info[9] = d->R;
+  });
+}
+
+int sfem_cuda_dist_phase(sfem_dist d, int phase, double* x, double* y, double* buf, void* stream) {
+  return guarded([&] {
+    require(d != nullptr, "dist_phase: null plan");
+    ck(cudaSetDevice(d->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    const int r = d->rank;
+    const long long lyR = d->ly[r] * d->R;
+    switch (phase) {
+      case SFEM_DIST_FORWARD_LOCAL:
+        launch_steps(d->phaseA, x, d->ctx, s, nullptr);
+        break;
+      case SFEM_DIST_PACK1:  // x-slab -> [L1*R][lx] (destination-major blocks)
+        ck(launch_slab_transpose(d->sv, x, buf, true, s), "slab transpose");
+        break;
+      case SFEM_DIST_UNPACK1:  // blocks [ly*R][lx_p] from each source p -> y rows, columns x0_p..
+        for (int p = 0; p < d->nranks; ++p) {
+          if (d->lx[p] == 0 || lyR == 0) continue;
+          ck(cudaMemcpy2DAsync(y + d->x0[p], d->ypitch * sizeof(double), buf + lyR * d->x0[p],
+                               d->lx[p] * sizeof(double), d->lx[p] * sizeof(double), lyR,
+                               cudaMemcpyDeviceToDevice, s),
+             "unpack1");
+        }
+        break;
+      case SFEM_DIST_AXIS0:
+        launch_steps(d->phaseB, y, d->ctx, s, nullptr);
+        break;
+      case SFEM_DIST_PACK2:  // y rows, columns x0_p.. -> blocks [ly*R][lx_p] for each destination p
+        for (int p = 0; p < d->nranks; ++p) {
+          if (d->lx[p] == 0 || lyR == 0) continue;
+          ck(cudaMemcpy2DAsync(buf + lyR * d->x0[p], d->lx[p] * sizeof(double), y + d->x0[p],
+                               d->ypitch * sizeof(double), d->lx[p] * sizeof(double), lyR,
+                               cudaMemcpyDeviceToDevice, s),
+             "pack2");
+        }
+        break;
+      case SFEM_DIST_UNPACK2:  // [L1*R][lx] (source-major blocks) -> x-slab
+        ck(launch_slab_transpose(d->sv, x, buf, false, s), "slab transpose");
+        break;
+      case SFEM_DIST_INVERSE_LOCAL:
+        launch_steps(d->phaseC, x, d->ctx, s, nullptr);
+        break;
+      default:
+        fail("dist_phase: unknown phase");
+    }
   });
 }
 

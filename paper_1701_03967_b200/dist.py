@@ -1,0 +1,175 @@
+"""Multi-GPU slab-decomposed solve over the C-ABI
+(sfem_cuda_dist_*), one process per GPU.
+
+The data path per solve on rank r:
+    FORWARD_LOCAL(x) -> PACK1 -> all_to_all -> UNPACK1 -> AXIS0(y)
+    -> PACK2 -> all_to_all (reverse counts) -> UNPACK2 -> INVERSE_LOCAL(x)
+x = the rank's axis-0 slab of the global dof tensor, y = its axis-1 slab with
+axis 0 contiguous.  The two all-to-alls are the only collectives (NCCL through
+torch.distributed on GPUs); everything else is the rank's own kernels.
+
+`partition` / `slab_*` restate the C++ slab arithmetic for the host side and
+for the CPU (gloo) tests.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import Context, Error, ProblemSpec, _check, default_context, lib
+
+PHASES = dict(forward_local=0, pack1=1, unpack1=2, axis0=3, pack2=4, unpack2=5, inverse_local=6)
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+def partition(n: int, parts: int):
+    """Balanced contiguous split of n rows: (offsets, lengths) (capi.cu `balanced`)."""
+    lens = [n // parts + (1 if r < n % parts else 0) for r in range(parts)]
+    offs = [sum(lens[:r]) for r in range(parts)]
+    return offs, lens
+
+
+@dataclass
+class SlabShape:
+    extents: List[int]
+    nranks: int
+    rank: int
+
+    @property
+    def R(self) -> int:
+        return int(np.prod(self.extents[2:])) if len(self.extents) > 2 else 1
+
+    def x(self):
+        offs, lens = partition(self.extents[0], self.nranks)
+        return offs[self.rank], lens[self.rank]
+
+    def y(self):
+        offs, lens = partition(self.extents[1], self.nranks)
+        return offs[self.rank], lens[self.rank]
+
+    def send_counts1(self) -> List[int]:
+        _, lx = self.x()
+        _, lys = partition(self.extents[1], self.nranks)
+        return [lx * ly * self.R for ly in lys]
+
+    def recv_counts1(self) -> List[int]:
+        _, ly = self.y()
+        _, lxs = partition(self.extents[0], self.nranks)
+        return [lx * ly * self.R for lx in lxs]
+
+
+class DistPlan:
+    """One rank's share of a slab-decomposed solve (sfem_cuda_dist_create)."""
+
+    def __init__(self, spec: ProblemSpec, nranks: int, rank: int, ctx: Optional[Context] = None):
+        spec.validate()
+        self.ctx = ctx or default_context()
+        self.spec = spec
+        N = spec.dimension
+        h = _vp()
+        coeffs = (ctypes.c_double * N)(*spec.coefficients) if spec.coefficients is not None else None
+        _check(lib.sfem_cuda_dist_create(self.ctx.handle, N, (ctypes.c_int * N)(*spec.orders),
+                                         (ctypes.c_int * N)(*spec.elements), (ctypes.c_double * N)(*spec.lengths),
+                                         ctypes.cast(coeffs, _dp) if coeffs is not None else None,
+                                         float(spec.shift), nranks, rank, ctypes.byref(h)))
+        self.handle = h
+        info = (ctypes.c_longlong * 10)()
+        sc = (ctypes.c_longlong * nranks)()
+        rc = (ctypes.c_longlong * nranks)()
+        _check(lib.sfem_cuda_dist_shape(h, info, sc, rc))
+        (self.x0, self.lx, self.y0, self.ly, self.x_elems, self.y_elems, self.buf_elems, self.xpitch,
+         self.ypitch, self.R) = list(info)
+        self.send_counts = list(sc)
+        self.recv_counts = list(rc)
+        self.nranks, self.rank = nranks, rank
+        self.extents = spec.extents()
+
+    def phase(self, name: str, x: int, y: int, buf: int, stream: int = 0):
+        _check(lib.sfem_cuda_dist_phase(self.handle, PHASES[name], _vp(x), _vp(y), _vp(buf), _vp(stream or None)))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.sfem_cuda_dist_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def solve_ranks(plans: Sequence[DistPlan], xs, bufs_a, bufs_b, ys, exchange):
+    """One distributed solve for the ranks in `plans` (one rank per process
+    with a real communicator, or every rank on one device for the loopback
+    check).  Per rank, CUDA tensors: x-slab, exchange buffers A (send 1 /
+    receive 2) and B (receive 1 / send 2), y-slab.  `exchange(step, plans,
+    sends, recvs)` performs the all-to-all of step 1 (send_counts ->
+    recv_counts) or step 2 (reversed).  Everything runs on torch's current
+    stream."""
+    import torch
+    stream = torch.cuda.current_stream().cuda_stream
+    ptr = lambda t: t.data_ptr()  # noqa: E731
+    for p, x, a, y in zip(plans, xs, bufs_a, ys):
+        p.phase("forward_local", ptr(x), ptr(y), ptr(a), stream)
+        p.phase("pack1", ptr(x), ptr(y), ptr(a), stream)
+    exchange(1, plans, bufs_a, bufs_b)
+    for p, x, b, y in zip(plans, xs, bufs_b, ys):
+        p.phase("unpack1", ptr(x), ptr(y), ptr(b), stream)
+        p.phase("axis0", ptr(x), ptr(y), ptr(b), stream)
+        p.phase("pack2", ptr(x), ptr(y), ptr(b), stream)
+    exchange(2, plans, bufs_b, bufs_a)
+    for p, x, a, y in zip(plans, xs, bufs_a, ys):
+        p.phase("unpack2", ptr(x), ptr(y), ptr(a), stream)
+        p.phase("inverse_local", ptr(x), ptr(y), ptr(a), stream)
+
+
+def _counts(p, step):
+    sc = p.send_counts if step == 1 else p.recv_counts
+    rc = p.recv_counts if step == 1 else p.send_counts
+    return list(sc), list(rc)
+
+
+def loopback_exchange(step, plans, sends, recvs):
+    """All-to-all among virtual ranks sharing one device (tensor copies)."""
+    P = len(plans)
+    for dst in range(P):
+        off_r = 0
+        for src in range(P):
+            sc, _ = _counts(plans[src], step)
+            off_s = sum(sc[:dst])
+            n = sc[dst]
+            if n:
+                recvs[dst][off_r:off_r + n].copy_(sends[src][off_s:off_s + n])
+            off_r += n
+
+
+def torch_exchange(step, plans, sends, recvs):
+    """All-to-all through torch.distributed (NCCL on GPUs, gloo on CPUs)."""
+    import torch.distributed as dist
+    (p,) = plans
+    sc, rc = _counts(p, step)
+    dist.all_to_all_single(recvs[0][:sum(rc)], sends[0][:sum(sc)], output_split_sizes=rc, input_split_sizes=sc)
+
+
+def allocate(plan: DistPlan, device="cuda"):
+    """Device buffers for one rank: (x, A, B, y)."""
+    import torch
+    mk = lambda n: torch.zeros(max(int(n), 1), dtype=torch.float64, device=device)  # noqa: E731
+    return mk(plan.x_elems), mk(plan.buf_elems), mk(plan.buf_elems), mk(plan.y_elems)
+
+
+def scatter_x(plan: DistPlan, x, load: np.ndarray):
+    """Copy the rank's axis-0 rows of a dense global dof tensor into its padded x-slab."""
+    import torch
+    ext = plan.extents
+    rows = load[plan.x0:plan.x0 + plan.lx].reshape(-1, ext[-1])
+    x.view(-1, plan.xpitch)[:rows.shape[0], :ext[-1]].copy_(torch.from_numpy(np.ascontiguousarray(rows)))
+
+
+def gather_x(plan: DistPlan, x) -> np.ndarray:
+    ext = plan.extents
+    rows = x.view(-1, plan.xpitch)[:, :ext[-1]].cpu().numpy()
+    return rows.reshape([plan.lx] + list(ext[1:]))

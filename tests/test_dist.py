@@ -1,0 +1,170 @@
+"""Slab-decomposed (multi-GPU) solve.
+
+CPU: world_size-2 (and 3) gloo runs of the real torch.distributed exchange
+with the per-rank phases emulated by the oracle (the host-side partition,
+pack/unpack and split-size logic of paper_1701_03967_b200/dist.py and
+csrc/dist.cu), compared with the single-process oracle solve.
+GPU: every rank's real kernels (sfem_cuda_dist_phase) with P virtual ranks
+on one device (loopback exchange), compared with the single-GPU solve."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, rel_l2
+from oracle import sfem_oracle as O
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class OracleRank:
+    """Rank-local phases of the slab solve on CPU tensors, restating
+    csrc/capi.cu (sfem_cuda_dist_phase) with the numpy oracle transforms."""
+
+    def __init__(self, orders, elements, lengths, shift, nranks, rank):
+        from paper_1701_03967_b200.dist import SlabShape, partition
+        self.orders, self.elements, self.lengths, self.shift = orders, elements, lengths, shift
+        self.ext = [n * K - 1 for n, K in zip(orders, elements)]
+        self.N = len(orders)
+        self.shape = SlabShape(self.ext, nranks, rank)
+        self.x0, self.lx = self.shape.x()
+        self.y0, self.ly = self.shape.y()
+        self.xoffs, self.xlens = partition(self.ext[0], nranks)
+        self.R = self.shape.R
+        self.send_counts = self.shape.send_counts1()
+        self.recv_counts = self.shape.recv_counts1()
+        self.tabs = [O.table(n, K) for n, K in zip(orders, elements)]
+        self.f = O.axis_scale_factors(lengths, elements)
+
+    def _along(self, x, axis, fn, t):
+        return np.moveaxis(fn(np.moveaxis(x, axis, -1), t), -1, axis)
+
+    def forward_local(self, x):
+        for a in range(self.N - 1, 0, -1):
+            x = self._along(x, a, O.decompose_weighted, self.tabs[a])
+        return x
+
+    def pack1(self, x):  # [lx][L1*R] -> [L1*R][lx]
+        return np.ascontiguousarray(x.reshape(self.lx, -1).T).reshape(-1)
+
+    def unpack1(self, buf):  # blocks [ly*R][lx_p] -> y[ly*R][L0]
+        lyR = self.ly * self.R
+        y = np.zeros((lyR, self.ext[0]))
+        for p, (o, n) in enumerate(zip(self.xoffs, self.xlens)):
+            y[:, o:o + n] = buf[lyR * o: lyR * (o + n)].reshape(lyR, n)
+        return y
+
+    def axis0(self, y):
+        t0 = self.tabs[0]
+        c = O.decompose_weighted(y, t0)  # along axis 0 (rows)
+        lead = [np.asarray(self.tabs[1].eigenvalues_coeff_order())[self.y0:self.y0 + self.ly]]
+        lead += [np.asarray(self.tabs[i].eigenvalues_coeff_order()) for i in range(2, self.N)]
+        base = np.full([len(v) for v in lead], self.shift)
+        for i, v in enumerate(lead):
+            shp = [1] * len(lead)
+            shp[i] = -1
+            base = base + self.f[i + 1] * v.reshape(shp)
+        denom = base.reshape(-1, 1) + self.f[0] * np.asarray(t0.eigenvalues_coeff_order()).reshape(1, -1)
+        return O.synthesize(c / denom, t0)
+
+    def pack2(self, y):
+        lyR = self.ly * self.R
+        buf = np.zeros(lyR * self.ext[0])
+        for o, n in zip(self.xoffs, self.xlens):
+            buf[lyR * o: lyR * (o + n)] = y[:, o:o + n].reshape(-1)
+        return buf
+
+    def unpack2(self, buf):
+        return np.ascontiguousarray(buf.reshape(-1, self.lx).T).reshape([self.lx] + self.ext[1:])
+
+    def inverse_local(self, x):
+        for a in range(1, self.N):
+            x = self._along(x, a, O.synthesize, self.tabs[a])
+        return x
+
+
+def _gloo_worker(rank, world, port, cfg, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orders, elements, lengths, shift = cfg
+    r = OracleRank(orders, elements, lengths, shift, world, rank)
+    f = np.random.default_rng(99).uniform(-1, 1, r.ext)
+    x = f[r.x0:r.x0 + r.lx].copy()
+    x = r.forward_local(x)
+    send = torch.from_numpy(r.pack1(x))
+    recv = torch.empty(sum(r.recv_counts), dtype=torch.float64)
+    dist.all_to_all_single(recv, send, output_split_sizes=r.recv_counts, input_split_sizes=r.send_counts)
+    y = r.axis0(r.unpack1(recv.numpy()))
+    send2 = torch.from_numpy(r.pack2(y))
+    recv2 = torch.empty(sum(r.send_counts), dtype=torch.float64)
+    dist.all_to_all_single(recv2, send2, output_split_sizes=r.send_counts, input_split_sizes=r.recv_counts)
+    x = r.inverse_local(r.unpack2(recv2.numpy()))
+    parts = [None] * world
+    dist.all_gather_object(parts, x)
+    if rank == 0:
+        np.save(out_path, np.concatenate(parts, axis=0))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cfg", [
+    (2, ([2, 3, 2], [4, 3, 5], [1.0, 1.0, 1.0], 0.5)),
+    (3, ([3, 2], [5, 4], [1.0, 2.0], 0.0)),
+    (2, ([1, 2, 2, 1], [5, 3, 2, 4], [1.0] * 4, 1.0)),
+])
+def test_gloo_slab_solve_matches_single_process(tmp_path, world, cfg):
+    out = str(tmp_path / "u.npy")
+    mp.spawn(_gloo_worker, args=(world, _free_port(), cfg, out), nprocs=world, join=True)
+    orders, elements, lengths, shift = cfg
+    ext = [n * K - 1 for n, K in zip(orders, elements)]
+    f = np.random.default_rng(99).uniform(-1, 1, ext)
+    want = O.solve_full_diagonalization(f, orders, elements, lengths, shift)
+    assert rel_l2(np.load(out), want) <= 1e-12
+
+
+def test_partition_and_counts_are_consistent():
+    from paper_1701_03967_b200.dist import SlabShape, partition
+    for n, P in ((575, 8), (7, 3), (9, 9), (1025, 4)):
+        offs, lens = partition(n, P)
+        assert sum(lens) == n and offs[0] == 0 and max(lens) - min(lens) <= 1
+    ext = [575, 575, 575]
+    shapes = [SlabShape(ext, 8, r) for r in range(8)]
+    # what r sends to s equals what s receives from r
+    for r in range(8):
+        for s in range(8):
+            assert shapes[r].send_counts1()[s] == shapes[s].recv_counts1()[r]
+    assert sum(sum(sh.send_counts1()) for sh in shapes) == int(np.prod(ext))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,orders,elements,lengths,shift", [
+    (1, [3, 3, 3], [8, 8, 8], [1.0] * 3, 0.0),
+    (2, [2, 3, 2], [8, 5, 9], [1.0, 2.0, 1.0], 0.5),
+    (3, [9, 9, 9], [4, 4, 4], [1.0] * 3, 0.0),
+    (4, [9, 9], [64, 64], [1.0, 1.0], 1.0),
+    (8, [9, 9, 9], [64, 64, 64], [1.0] * 3, 0.0),
+])
+def test_loopback_slab_solve_matches_single_gpu(sfem, P, orders, elements, lengths, shift):
+    from paper_1701_03967_b200 import dist as D
+    spec = sfem.ProblemSpec(len(orders), lengths, elements, orders, shift)
+    f = np.random.default_rng(P).uniform(-1, 1, spec.extents())
+    want, _ = sfem.solve_dof(spec, f)
+    plans = [D.DistPlan(spec, P, r) for r in range(P)]
+    bufs = [D.allocate(p) for p in plans]
+    for p, (x, a, b, y) in zip(plans, bufs):
+        D.scatter_x(p, x, f)
+    D.solve_ranks(plans, [b[0] for b in bufs], [b[1] for b in bufs], [b[2] for b in bufs], [b[3] for b in bufs],
+                  D.loopback_exchange)
+    torch.cuda.synchronize()
+    got = np.concatenate([D.gather_x(p, b[0]) for p, b in zip(plans, bufs)], axis=0)
+    assert rel_l2(got, want) <= 1e-13
