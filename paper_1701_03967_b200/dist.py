@@ -110,7 +110,15 @@ def solve_ranks(plans: Sequence[DistPlan], xs, bufs_a, bufs_b, ys, exchange):
     recv_counts) or step 2 (reversed).  Everything runs on torch's current
     stream."""
     import torch
-    stream = torch.cuda.current_stream().cuda_stream
+    # One stream for kernels and exchanges: the plans' context stream (a NULL
+    # stream argument would select it inside the library while torch's copies
+    # ran on the legacy default stream, unordered).
+    ext = torch.cuda.ExternalStream(plans[0].ctx.stream)
+    with torch.cuda.stream(ext):
+        _solve_ranks(plans, xs, bufs_a, bufs_b, ys, exchange, ext.cuda_stream)
+
+
+def _solve_ranks(plans, xs, bufs_a, bufs_b, ys, exchange, stream):
     ptr = lambda t: t.data_ptr()  # noqa: E731
     for p, x, a, y in zip(plans, xs, bufs_a, ys):
         p.phase("forward_local", ptr(x), ptr(y), ptr(a), stream)
