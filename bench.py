@@ -182,6 +182,89 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_distributed(args, world, rank, local, dist):
+    """N > 1: ONE global problem, slab-decomposed over the ranks (axis-0 slabs,
+    two NCCL all-to-all transposes per solve; paper_1701_03967_b200/dist.py).
+    Strong scaling: value = global unknowns / max-over-ranks time."""
+    import ctypes
+    import torch
+    import paper_1701_03967_b200 as sfem
+    from paper_1701_03967_b200 import dist as D
+
+    orders, elements, lengths, coeffs, shift, desc = CONFIGS[args.config]
+    spec = sfem.ProblemSpec(len(orders), lengths, elements, orders, shift, coefficients=coeffs)
+    ctx = sfem.Context(local)
+    plan = D.DistPlan(spec, world, rank, ctx)
+    U = int(np.prod(plan.extents))
+    x, a, b, y = D.allocate(plan)
+    rows_local = plan.lx * int(np.prod(plan.extents[1:-1]))
+    f_local = np.random.default_rng(1000 + rank).uniform(-1.0, 1.0, (rows_local, plan.extents[-1]))
+    x.view(-1, plan.xpitch)[:rows_local, :plan.extents[-1]].copy_(torch.from_numpy(f_local))
+    ext = torch.cuda.ExternalStream(ctx.stream)
+
+    def solve():
+        D.solve_ranks([plan], [x], [a], [b], [y], D.torch_exchange)
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(dist, world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        ev0.record(ext)
+        for _ in range(args.steps):
+            solve()
+        ev1.record(ext)
+        torch.cuda.synchronize()
+    barrier(dist, world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), dist, world)
+    value = U * args.steps / (ms * 1e-3)
+    ms_step = ms / args.steps
+    peaks, peak_kind = measured_peaks()
+    # per-rank HBM bytes per solve: 2N-1 sweeps + 2 transposes + 2 2-D copies (read + write each)
+    local_u = U / world
+    sweep_bytes = 16.0 * local_u * (2 * len(orders) - 1)
+    copy_bytes = 16.0 * local_u * 4
+    achieved = (sweep_bytes + copy_bytes) / (ms_step * 1e-3) / 1e9
+    a2a_bytes = 2 * 8.0 * sum(c for i, c in enumerate(plan.send_counts) if i != rank)
+
+    # end to end: each rank moves its own slab host -> device -> host
+    h_in = torch.from_numpy(f_local).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    barrier(dist, world)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        with torch.cuda.stream(ext):
+            x.view(-1, plan.xpitch)[:rows_local, :plan.extents[-1]].copy_(h_in, non_blocking=True)
+        solve()
+        with torch.cuda.stream(ext):
+            h_out.copy_(x.view(-1, plan.xpitch)[:rows_local, :plan.extents[-1]], non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, dist, world)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "unknowns": U, "extents": plan.extents,
+                       "parallelism": f"slab x{world} (axis-0 slabs, 2 NCCL all-to-all per solve)",
+                       "l2_flush": "none needed: tensors > L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "whole per-rank solve (sweeps + transposes)",
+                         "nvlink_bytes_per_rank_per_solve": a2a_bytes},
+            "cpu_baseline": None,
+            "e2e": {"value": U / e2e_s, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * int(f_local.size) * world,
+                    "d2h_bytes_per_step": 8 * int(f_local.size) * world, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": 7 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,12 +274,24 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-single", action="store_true",
+                    help="exercise the slab-decomposed path on one GPU (1-rank NCCL group)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     args.steps = max(1, min(args.steps, 150))  # solutions shrink ~30x per in-place solve
 
     world, rank, local, dist = dist_setup()
+    if args.dist_single and world == 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as tdist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29555")
+        torch.cuda.set_device(0)
+        tdist.init_process_group("nccl", rank=0, world_size=1)
+        run_distributed(args, 1, 0, 0, tdist)
+        tdist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, world, rank)
         if world > 1:
@@ -207,6 +302,14 @@ def main():
     import paper_1701_03967_b200 as sfem
 
     torch.cuda.set_device(local)
+    if world > 1:
+        try:
+            run_distributed(args, world, rank, local, dist)
+            dist.destroy_process_group()
+            return
+        except Exception as e:  # reported in the JSON line; replicas below
+            print(f"[bench] slab-decomposed solve failed on rank {rank}: {e!r}; running replicas", file=sys.stderr)
+            args.dist_error = repr(e)
     orders, elements, lengths, coeffs, shift, desc = CONFIGS[args.config]
     spec = sfem.ProblemSpec(len(orders), lengths, elements, orders, shift, coefficients=coeffs)
     ctx = sfem.Context(local)
@@ -305,6 +408,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "unknowns_per_gpu": U, "extents": ext, "device_pitch": plan.pitch,
                        "l2_flush": "none needed: 1.52 GB tensor > 126 MB L2", "parallelism": f"replicas x{world}",
+                       "dist_error": getattr(args, "dist_error", None),
                        "schedule": "2N-1 sweeps: fwd axes 0..N-2, fused fwd+divide+inv last axis, inv axes N-2..0"},
             "roofline": roofline,
             "cpu_baseline": cpu,
