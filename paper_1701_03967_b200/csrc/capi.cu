@@ -387,6 +387,7 @@ struct sfem_plan_s {
   long long rows = 0;  // product of leading extents
   std::vector<Step> steps;
   double* dwork = nullptr;
+  double* dstage = nullptr;  // dense host-transfer staging
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> kev;
   bool use_fast = true;
@@ -784,6 +785,7 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
     if (!p) return;
     cudaSetDevice(p->ctx->device);
     if (p->dwork) cudaFree(p->dwork);
+    if (p->dstage) cudaFree(p->dstage);
     for (auto& t : p->owned)
       if (t->dbuf) cudaFree(t->dbuf);
     for (auto e : p->ev)
@@ -829,21 +831,26 @@ int sfem_cuda_solve_host(sfem_plan p, const double* h_load, double* h_u, double*
   return guarded([&] {
     require(p && h_load && h_u, "solve_host: null argument");
     ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
-    // Padded device copy (pitch: 32-byte rows, TMA-compatible); the copy
-    // engine does the re-pitching.
+    // Host <-> device as dense 1-D copies (full PCIe rate), re-pitched on the
+    // device into the padded (TMA-compatible) work tensor.
     const long long last = p->ext[p->dim - 1];
     const long long pitch = (last + 3) & ~3LL;
     ensure_work(p);
     cudaStream_t s = p->ctx->stream;
-    ck(cudaMemcpy2DAsync(p->dwork, pitch * sizeof(double), h_load, last * sizeof(double), last * sizeof(double),
-                         p->rows, cudaMemcpyHostToDevice, s),
-       "H2D");
+    const size_t dense = static_cast<size_t>(p->rows) * last;
+    if (!p->dstage) ck(cudaMalloc(&p->dstage, dense * sizeof(double)), "cudaMalloc(stage)");
+    double* stage = p->dstage;
+    ck(cudaMemcpyAsync(stage, h_load, dense * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    ck(cudaMemcpy2DAsync(p->dwork, pitch * sizeof(double), stage, last * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyDeviceToDevice, s),
+       "repitch");
     ck(cudaEventRecord(p->ev[0], s), "event");
     run_steps(p, p->dwork, pitch, s, false);
     ck(cudaEventRecord(p->ev[1], s), "event");
-    ck(cudaMemcpy2DAsync(h_u, last * sizeof(double), p->dwork, pitch * sizeof(double), last * sizeof(double),
-                         p->rows, cudaMemcpyDeviceToHost, s),
-       "D2H");
+    ck(cudaMemcpy2DAsync(stage, last * sizeof(double), p->dwork, pitch * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyDeviceToDevice, s),
+       "repitch");
+    ck(cudaMemcpyAsync(h_u, stage, dense * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
     if (seconds) *seconds = event_seconds(p->ev[0], p->ev[1]);
   });
