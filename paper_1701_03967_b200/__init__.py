@@ -76,6 +76,7 @@ _SIGS = [
     ("sfem_cuda_solve_device", ctypes.c_int, [_vp, _vp, ctypes.c_longlong, _vp]),
     ("sfem_cuda_solve_host", ctypes.c_int, [_vp, _dp, _dp, _dp]),
     ("sfem_cuda_solve_classes", ctypes.c_int, [_vp, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _dp]),
+    ("sfem_cuda_solve_host_batch", ctypes.c_int, [_vp, ctypes.c_longlong, ctypes.POINTER(_dp), ctypes.POINTER(_dp)]),
     ("sfem_cuda_solve_device_timed", ctypes.c_int,
      [_vp, _vp, ctypes.c_longlong, ctypes.c_int, _dp, _dp]),
     ("sfem_cuda_dist_create", ctypes.c_int,
@@ -399,6 +400,14 @@ class Plan:
         sec = ctypes.c_double()
         _check(lib.sfem_cuda_solve_host(self.handle, _dptr(load), _dptr(u), ctypes.byref(sec)))
         return u, sec.value
+
+    def solve_host_batch(self, loads, outs):
+        """Pipelined solves of several host loads (sfem_cuda_solve_host_batch).
+        `loads` / `outs`: sequences of raw host pointers (ints) or float64 arrays."""
+        def ptrs(xs):
+            return (_dp * len(xs))(*[ctypes.cast(ctypes.c_void_p(x if isinstance(x, int) else x.ctypes.data), _dp)
+                                     for x in xs])
+        _check(lib.sfem_cuda_solve_host_batch(self.handle, len(loads), ptrs(loads), ptrs(outs)))
 
     def solve_device(self, dev_ptr: int, pitch: Optional[int] = None, stream: int = 0):
         _check(lib.sfem_cuda_solve_device(self.handle, ctypes.c_void_p(dev_ptr),

@@ -388,6 +388,11 @@ struct sfem_plan_s {
   std::vector<Step> steps;
   double* dwork = nullptr;
   double* dstage = nullptr;  // dense host-transfer staging
+  // pipelined host solves (sfem_cuda_solve_host_batch): two in-flight slots
+  double* pwork[2] = {nullptr, nullptr};
+  double* pstage[2] = {nullptr, nullptr};
+  cudaStream_t pin = nullptr, pout = nullptr;
+  cudaEvent_t e_in[2] = {nullptr, nullptr}, e_comp[2] = {nullptr, nullptr}, e_out[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> kev;
   bool use_fast = true;
@@ -786,6 +791,15 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
     cudaSetDevice(p->ctx->device);
     if (p->dwork) cudaFree(p->dwork);
     if (p->dstage) cudaFree(p->dstage);
+    for (int b = 0; b < 2; ++b) {
+      if (p->pwork[b]) cudaFree(p->pwork[b]);
+      if (p->pstage[b]) cudaFree(p->pstage[b]);
+      if (p->e_in[b]) cudaEventDestroy(p->e_in[b]);
+      if (p->e_comp[b]) cudaEventDestroy(p->e_comp[b]);
+      if (p->e_out[b]) cudaEventDestroy(p->e_out[b]);
+    }
+    if (p->pin) cudaStreamDestroy(p->pin);
+    if (p->pout) cudaStreamDestroy(p->pout);
     for (auto& t : p->owned)
       if (t->dbuf) cudaFree(t->dbuf);
     for (auto e : p->ev)
@@ -853,6 +867,52 @@ int sfem_cuda_solve_host(sfem_plan p, const double* h_load, double* h_u, double*
     ck(cudaMemcpyAsync(h_u, stage, dense * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
     if (seconds) *seconds = event_seconds(p->ev[0], p->ev[1]);
+  });
+}
+
+int sfem_cuda_solve_host_batch(sfem_plan p, long long count, const double* const* h_loads, double* const* h_us) {
+  return guarded([&] {
+    require(p && h_loads && h_us && count >= 0, "solve_host_batch: bad argument");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    const long long last = p->ext[p->dim - 1];
+    const long long pitch = (last + 3) & ~3LL;
+    const size_t dense = static_cast<size_t>(p->rows) * last;
+    const size_t padded = static_cast<size_t>(p->rows) * pitch;
+    if (!p->pin) {
+      ck(cudaStreamCreateWithFlags(&p->pin, cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithFlags(&p->pout, cudaStreamNonBlocking), "stream");
+      for (int b = 0; b < 2; ++b) {
+        ck(cudaMalloc(&p->pwork[b], padded * sizeof(double)), "cudaMalloc(work)");
+        ck(cudaMalloc(&p->pstage[b], dense * sizeof(double)), "cudaMalloc(stage)");
+        ck(cudaEventCreateWithFlags(&p->e_in[b], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&p->e_comp[b], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&p->e_out[b], cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(p->e_out[b], p->pout), "event");
+      }
+    }
+    cudaStream_t sc = p->ctx->stream;
+    // problem i uses slot b = i % 2: H2D of i+1 overlaps the solve of i and
+    // the D2H of i-1 (three streams; PCIe moves both directions at once)
+    for (long long i = 0; i < count; ++i) {
+      const int b = static_cast<int>(i & 1);
+      ck(cudaStreamWaitEvent(p->pin, p->e_out[b], 0), "wait");
+      ck(cudaMemcpyAsync(p->pstage[b], h_loads[i], dense * sizeof(double), cudaMemcpyHostToDevice, p->pin), "H2D");
+      ck(cudaEventRecord(p->e_in[b], p->pin), "event");
+      ck(cudaStreamWaitEvent(sc, p->e_in[b], 0), "wait");
+      ck(cudaMemcpy2DAsync(p->pwork[b], pitch * sizeof(double), p->pstage[b], last * sizeof(double),
+                           last * sizeof(double), p->rows, cudaMemcpyDeviceToDevice, sc),
+         "repitch");
+      run_steps(p, p->pwork[b], pitch, sc, false);
+      ck(cudaMemcpy2DAsync(p->pstage[b], last * sizeof(double), p->pwork[b], pitch * sizeof(double),
+                           last * sizeof(double), p->rows, cudaMemcpyDeviceToDevice, sc),
+         "repitch");
+      ck(cudaEventRecord(p->e_comp[b], sc), "event");
+      ck(cudaStreamWaitEvent(p->pout, p->e_comp[b], 0), "wait");
+      ck(cudaMemcpyAsync(h_us[i], p->pstage[b], dense * sizeof(double), cudaMemcpyDeviceToHost, p->pout), "D2H");
+      ck(cudaEventRecord(p->e_out[b], p->pout), "event");
+    }
+    ck(cudaStreamSynchronize(p->pout), "sync");
+    ck(cudaStreamSynchronize(sc), "sync");
   });
 }
 

@@ -294,3 +294,14 @@ def test_long_lines_match_oracle(sfem, n, K):
     x = np.random.default_rng(K).standard_normal((3, n * K - 1))
     for op, fn in ((0, O.decompose_weighted), (1, O.decompose), (2, O.synthesize)):
         assert rel_l2(sfem.lines(t, op, x), fn(x, ot)) <= TOL
+
+
+def test_pipelined_host_batch_matches_single_solves(sfem):
+    spec = sfem.ProblemSpec(3, [1.0] * 3, [16, 16, 16], [9, 9, 9], 0.5)
+    plan = sfem.Plan(spec)
+    loads = [np.random.default_rng(s).uniform(-1, 1, spec.extents()) for s in range(5)]
+    outs = [np.empty_like(x) for x in loads]
+    plan.solve_host_batch(loads, outs)
+    for x, u in zip(loads, outs):
+        want, _ = plan.solve_host(x)
+        assert np.array_equal(u, want)
