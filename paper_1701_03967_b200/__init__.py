@@ -31,7 +31,9 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libsfem_b200.so")
+# SFEM_LIB: alternative build of the same library (kernel-variant experiments,
+# tools/variants.sh); default the in-tree build.
+lib_path = os.environ.get("SFEM_LIB") or os.path.join(_HERE, "libsfem_b200.so")
 
 DECOMPOSE_WEIGHTED, DECOMPOSE, SYNTHESIZE = 0, 1, 2
 
