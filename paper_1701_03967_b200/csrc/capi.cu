@@ -363,6 +363,8 @@ void launch_steps(std::vector<Step>& steps, double* data, sfem_ctx ctx, cudaStre
       ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
     } else if (s.use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous)) {
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
+    } else if (s.use_fast && has_mid_sweep(dt.n, dt.K)) {
+      ck(launch_sweep_mid(dt, s.ls, s.mode, kWeighted, sym, stream), "mid sweep launch");
     } else {
       double* gw = nullptr;
       if (s.gwork) gw = scratch_for(ctx, sweep_work_doubles(dt, s.B) * ((s.ls.nlines + s.B - 1) / s.B));
@@ -708,6 +710,8 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
     const int analysis = op == SFEM_OP_DECOMPOSE ? kDirect : kWeighted;
     if (fast_enabled() && has_fast_sweep(t->dev.n, t->dev.K, mode, 1)) {
       ck(launch_sweep_fast(t->dev, ls, mode, analysis, nullptr, s), "lines launch (fast)");
+    } else if (fast_enabled() && has_mid_sweep(t->dev.n, t->dev.K)) {
+      ck(launch_sweep_mid(t->dev, ls, mode, analysis, nullptr, s), "lines launch (mid)");
     } else {
       bool gwork = false;
       const int B = choose_tile(t->dev, count, &gwork);

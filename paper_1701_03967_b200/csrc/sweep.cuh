@@ -87,6 +87,11 @@ cudaError_t launch_sweep_fast(const DevTable& t, const LineSet& lines, int mode,
                               const SymbolInfo* sym, cudaStream_t stream);
 bool has_fast_sweep(int n, int K, int mode, int contiguous);
 
+// Mid-length line kernels (sweep_mid.cu) for the (n, K) they were compiled for.
+bool has_mid_sweep(int n, int K);
+cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& lines, int mode, int analysis,
+                             const SymbolInfo* sym, cudaStream_t stream);
+
 // Launch one sweep over `lines` with tiles of B lines.
 cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int analysis,
                          const SymbolInfo* sym, int B, cudaStream_t stream, double* gwork = nullptr);

@@ -1,0 +1,682 @@
+// Sweep kernels for mid-length lines (n*K ~ 1000-10000): C5's (n, K) in
+// {(1,1024), (2,512), (4,256), (9,114)} and C3's (9,1024).
+//
+// Same mathematics as sweep.cu (reference eigenbasis.cpp:63-225),
+// specialised at compile time on (n, K, lines per tile B, threads) and laid
+// out for one large tile per CTA:
+//   * one shared-memory region is reused in place for every stage: the tile
+//     T[pos][b], the FFT buffer W[t][job] (complex) and the per-frequency slots
+//     S, which are stored at the tile positions of the coefficients they
+//     become (S row r <-> tile position m + r).  Stages that permute data move
+//     it through registers ("bridges": every thread loads its items, barrier,
+//     every thread stores);
+//   * FFTs are in-place Stockham passes with compile-time radices (16/8/4/2
+//     register butterflies, odd radices 3 and 19 as direct DFTs);
+//   * the n x n mix of a frequency touches only that frequency's n slots of a
+//     line, so it runs in place per (k, line) item; the last-axis kernel does
+//     forward mix, symbol divide and inverse mix of an item in registers;
+//   * the zero-frequency centre sums (eigenbasis.cpp:31-40) are chunked over
+//     all threads and reduced in a fixed order (deterministic).
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "fft_reg.cuh"
+#include "sweep.cuh"
+
+namespace sfem_b200 {
+namespace mid {
+
+using namespace reg;
+
+#include "phase_timing.cuh"
+
+// ROWS: tile stored line-major T[b][pos] (line pitch LP, odd: conflict-free
+// for lanes over lines), used when lines are rows of the tensor; otherwise
+// position-major T[pos][b] (strided axes, lanes over the 8 adjacent lines).
+template <int NN, int K, int BB, int TH, bool ROWS_>
+struct Cfg {
+  static constexpr int n = NN, m = NN - 1, half = m / 2, ne = NN / 2, N = K, L = NN * K - 1;
+  static constexpr bool ROWS = ROWS_;
+  static constexpr int LP = L | 1;
+  static constexpr int PSTR = ROWS ? 1 : BB;  // position stride in the tile
+  __device__ __forceinline__ static constexpr int ix(int pos, int b) { return ROWS ? b * LP + pos : pos * BB + b; }
+  static constexpr int B = BB, Bh = (BB + 1) / 2, Bm = (m & 1) ? Bh : 0;
+  static constexpr int NPAIR = B * half;
+  static constexpr int J = NPAIR + Bm + 2 * Bh;
+  static constexpr int THREADS = TH;
+  static constexpr int WD = 2 * J * K;  // FFT buffer (doubles)
+  static constexpr int TD = (ROWS ? LP : L) * B;  // tile (doubles)
+  static constexpr int REGION = WD > TD ? WD : TD;
+  static constexpr int NCEN = m * B;  // centre sums
+  static constexpr int CHUNKS = NCEN > 0 ? (TH / NCEN > 0 ? TH / NCEN : 1) : 1;
+  static constexpr int ECH = (K + CHUNKS - 1) / CHUNKS;  // elements per chunk
+  static constexpr int C0_OFF = REGION;
+  static constexpr int PS_OFF = C0_OFF + (NCEN > 0 ? NCEN : 1);
+  static constexpr int BASE_OFF = PS_OFF + (NCEN > 0 ? CHUNKS * NCEN : 1);
+  static constexpr int TOTAL = BASE_OFF + B;
+  static constexpr size_t SMEM = static_cast<size_t>(TOTAL) * sizeof(double);
+};
+
+// Radix plans (product = K), chosen so that one pass keeps at most ~24
+// complex values per thread in flight.
+template <int K>
+struct Plan;
+template <>
+struct Plan<1024> {
+  static constexpr int NP = 4;
+  static constexpr int R[4] = {8, 8, 4, 4};
+};
+template <>
+struct Plan<512> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 8, 8};
+};
+template <>
+struct Plan<256> {
+#if SFEM_MID_TH256
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {4, 8, 8};
+#else
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {16, 16};
+#endif
+};
+template <>
+struct Plan<114> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {2, 3, 19};
+};
+
+__device__ __forceinline__ int makhoul_src(int t, int N) { return (2 * t < N) ? 2 * t : 2 * N - 1 - 2 * t; }
+
+// Direct DFT of odd length R with roots from the K-point twiddle table.
+template <int R, int K>
+__device__ __forceinline__ void dft_direct(double2 (&x)[R], const double2* __restrict__ tw) {
+  double2 y[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) {
+    double2 s = x[0];
+#pragma unroll
+    for (int q = 1; q < R; ++q) s = c_add(s, c_mul(x[q], __ldg(tw + ((q * p) % R) * (K / R))));
+    y[p] = s;
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p) x[p] = y[p];
+}
+
+template <int R, int K>
+__device__ __forceinline__ void dft(double2 (&x)[R], const double2* __restrict__ tw) {
+  if constexpr (R == 2 || R == 4 || R == 8 || R == 16)
+    Dft<R>::run(x);
+  else if constexpr (R == 3) {
+    // exp(-2 pi i/3) = -1/2 - i sqrt(3)/2
+    constexpr double s3 = 0.86602540378443864676;
+    const double2 a = x[0], b = x[1], c = x[2];
+    const double2 t = c_add(b, c), d = c_sub(b, c);
+    x[0] = c_add(a, t);
+    const double2 u = make_double2(fma(-0.5, t.x, a.x), fma(-0.5, t.y, a.y));
+    // -i sqrt3/2 d
+    const double2 v = make_double2(s3 * d.y, -s3 * d.x);
+    x[1] = c_add(u, v);
+    x[2] = c_sub(u, v);
+  } else {
+    dft_direct<R, K>(x, tw);
+  }
+}
+
+// One in-place Stockham pass of radix R after NS points are done, over all J
+// interleaved jobs of W[t * J + job].
+template <class C, int R, int NS>
+__device__ __forceinline__ void fft_pass(double2* W, const double2* __restrict__ tw) {
+  constexpr int N = C::N, J = C::J, NR = N / R, ITEMS = NR * J;
+  constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  constexpr int TSTEP = N / (NS * R);
+  double2 v[IPT][R];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) {
+      const int job = it % J, j = it / J, k = j % NS;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        double2 a = W[(j + q * NR) * J + job];
+        if (NS > 1 && q > 0) a = c_mul(a, __ldg(tw + (q * k * TSTEP) % N));
+        v[i][q] = a;
+      }
+      dft<R, N>(v[i], tw);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) {
+      const int job = it % J, j = it / J, k = j % NS;
+      const int outb = (j / NS) * NS * R + k;
+#pragma unroll
+      for (int pp = 0; pp < R; ++pp) W[(outb + pp * NS) * J + job] = v[i][pp];
+    }
+  }
+  __syncthreads();
+}
+
+template <class C, int P = 0, int NS = 1>
+__device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
+  using PL = Plan<C::N>;
+  if constexpr (P < PL::NP) {
+    constexpr int R = PL::R[P];
+    fft_pass<C, R, NS>(W, tw);
+    fft<C, P + 1, NS * R>(W, tw);
+  }
+}
+
+// ------------------------------------------------------------ forward fill
+// W[t][job] from the tile (bridge), plus the chunked centre partial sums.
+template <class C>
+__device__ __forceinline__ void forward_fill(double* R, double* PS, const double2* __restrict__ om) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  const double* T = R;
+  double2 z[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    z[i] = make_double2(0.0, 0.0);
+    if (it < ITEMS) {
+      const int job = it % J, tt = it / J;
+      if (job < NPAIR) {
+        const int ii = job / B, b = job % B;
+        const int e = makhoul_src(tt, N);
+        const double ri = T[C::ix(e * n + ii, b)], rr = T[C::ix(e * n + m - 1 - ii, b)];
+        double gg = ri + rr;
+        if (e & 1) gg = -gg;
+        z[i] = make_double2(ri - rr, gg);
+      } else if (job < NPAIR + C::Bm) {
+        const int b = job - NPAIR, b2 = b + Bh;
+        const int e = makhoul_src(tt, N);
+        double g1 = T[C::ix(e * n + C::half, b)];
+        double g2 = b2 < B ? T[C::ix(e * n + C::half, b2)] : 0.0;
+        if (e & 1) {
+          g1 = -g1;
+          g2 = -g2;
+        }
+        z[i] = make_double2(g1, g2);
+      } else {
+        const int jb = job - NPAIR - C::Bm;
+        const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+        if (tt > 0) {
+          z[i] = make_double2(T[C::ix(tt * n - 1, b)], b2 < B ? T[C::ix(tt * n - 1, b2)] : 0.0);
+          if (which) z[i] = c_mul(z[i], __ldg(om + tt));
+        }
+      }
+    }
+  }
+  // centre partials: sum (i, b) over elements [c * ECH, (c+1) * ECH)
+  double part = 0.0;
+  const int cit = threadIdx.x;
+  if constexpr (C::NCEN > 0) {
+    if (cit < C::CHUNKS * C::NCEN) {
+      const int s = cit % C::NCEN, c = cit / C::NCEN;
+      const int ii = s / B, b = s % B;
+      const int e0 = c * C::ECH, e1 = min(N, e0 + C::ECH);
+      for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ix(e * n + m - 1 - ii, b)] : T[C::ix(e * n + ii, b)];
+    }
+  }
+  __syncthreads();
+  double2* W = reinterpret_cast<double2*>(R);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) W[it] = z[i];  // it = tt * J + job
+  }
+  if (C::NCEN > 0 && cit < C::CHUNKS * C::NCEN) PS[cit] = part;  // NCEN = 0: no centre (n = 1)
+  __syncthreads();
+}
+
+// C0[s] = sum over chunks in order.
+template <class C>
+__device__ __forceinline__ void centre_reduce(const double* PS, double* C0) {
+  for (int s = threadIdx.x; s < C::NCEN; s += C::THREADS) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < C::CHUNKS; ++c) acc += PS[c * C::NCEN + s];
+    C0[s] = acc;
+  }
+}
+
+// ------------------------------------------------------------ forward post
+// FFT results -> slots S (at tile positions m + (k-1) n + s), bridge.
+template <class C>
+__device__ __forceinline__ void forward_post(double* R, const double2* __restrict__ mk) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  constexpr int ITEMS = (N - 1) * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  const double2* Z = reinterpret_cast<const double2*>(R);
+  double v1[IPT], v2[IPT];
+  int i1[IPT], i2[IPT];  // destination indices (-1: none)
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    i1[i] = -1;
+    i2[i] = -1;
+    v1[i] = v2[i] = 0.0;
+    if (it < ITEMS) {
+      const int job = it % J, k = 1 + it / J;
+      if (job < NPAIR + C::Bm) {
+        const double2 zk = Z[k * J + job], zc = Z[(N - k) * J + job];
+        const double2 w = __ldg(mk + k);
+        // r1 = Re(mk_k V1), r2 = Re(mk_k V2), V1 = (Z_k + conj Z_{N-k})/2, V2 = (Z_k - conj Z_{N-k})/(2i)
+        const double a1 = 0.5 * (zk.x + zc.x), b1 = 0.5 * (zk.y - zc.y);
+        const double a2 = 0.5 * (zk.y + zc.y), b2 = -0.5 * (zk.x - zc.x);
+        v1[i] = w.x * a1 - w.y * b1;
+        v2[i] = w.x * a2 - w.y * b2;
+        if (job < NPAIR) {
+          const int ii = job / B, b = job % B;
+          i1[i] = C::ix(m + (k - 1) * n + 1 + C::ne + ii, b);  // H_k
+          i2[i] = C::ix(m + (N - k - 1) * n + 1 + ii, b);      // G_{N-k}
+        } else {
+          const int b = job - NPAIR, bb = b + Bh;
+          i1[i] = C::ix(m + (N - k - 1) * n + 1 + C::half, b);
+          if (bb < B) i2[i] = C::ix(m + (N - k - 1) * n + 1 + C::half, bb);
+        }
+      } else {
+        const int jb = job - NPAIR - C::Bm;
+        const int b = jb % Bh, which = jb / Bh, bb = b + Bh;
+        if ((k & 1) == which) {
+          double2 d;
+          if (!which) {
+            const int kp = k / 2;
+            d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
+          } else {
+            const int kp = (k - 1) / 2;
+            d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
+          }
+          // X = d / (2i)
+          v1[i] = 0.5 * d.y;
+          v2[i] = -0.5 * d.x;
+          i1[i] = C::ix(m + (k - 1) * n, b);
+          if (bb < B) i2[i] = C::ix(m + (k - 1) * n, bb);
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    if (i1[i] >= 0) R[i1[i]] = v1[i];
+    if (i2[i] >= 0) R[i2[i]] = v2[i];
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ mixes
+// Per (k >= 1, line) item, in place at tile positions m + (k-1) n + [0, n):
+//   MODE kForward:             c = Mf v
+//   MODE kInverse:             u = Mi c
+//   MODE kForwardDivideInverse u = Mi (Mf v / denom)
+// Items (K-1)*B .. (K-1)*B + B - 1 are the centre blocks of the lines.
+template <class C, int MODE>
+__device__ __forceinline__ void mix(double* T, double* C0, const double* __restrict__ mixF,
+                                    const double* __restrict__ e0F, const double* __restrict__ mixI,
+                                    const double* __restrict__ e0I, const double* base,
+                                    const double* __restrict__ eig, double f_last) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B;
+  constexpr int ITEMS = (N - 1) * B + B;
+  for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+    if (it < (N - 1) * B) {
+      const int k = 1 + it / B, b = it % B;
+      double* p = T + C::ix(m + (k - 1) * n, b);
+      double v[n], c[n];
+#pragma unroll
+      for (int s = 0; s < n; ++s) v[s] = p[s * C::PSTR];
+      if (MODE != kInverse) {
+        const double* M = mixF + static_cast<size_t>(k - 1) * n * n;
+#pragma unroll
+        for (int l = 0; l < n; ++l) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < n; ++s) acc = fma(__ldg(M + l * n + s), v[s], acc);
+          if (MODE == kForwardDivideInverse) acc = acc / (base[b] + f_last * __ldg(eig + m + (k - 1) * n + l));
+          c[l] = acc;
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < n; ++l) c[l] = v[l];
+      }
+      if (MODE != kForward) {
+        const double* M = mixI + static_cast<size_t>(k - 1) * n * n;
+#pragma unroll
+        for (int s = 0; s < n; ++s) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < n; ++l) acc = fma(__ldg(M + s * n + l), c[l], acc);
+          v[s] = acc;
+        }
+#pragma unroll
+        for (int s = 0; s < n; ++s) p[s * C::PSTR] = v[s];
+      } else {
+#pragma unroll
+        for (int l = 0; l < n; ++l) p[l * C::PSTR] = c[l];
+      }
+    } else if (m > 0) {
+      // centre block of line b: coefficients l < m (k = 0)
+      const int b = it - (N - 1) * B;
+      double c[m > 0 ? m : 1];
+      if (MODE != kInverse) {
+#pragma unroll
+        for (int l = 0; l < m; ++l) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < m; ++i) acc = fma(C0[i * B + b], __ldg(e0F + i * m + l), acc);
+          if (MODE == kForwardDivideInverse) acc = acc / (base[b] + f_last * __ldg(eig + l));
+          c[l] = acc;
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < m; ++l) c[l] = T[C::ix(l, b)];
+      }
+      if (MODE == kForward) {
+#pragma unroll
+        for (int l = 0; l < m; ++l) T[C::ix(l, b)] = c[l];
+      } else {
+        // centre of the synthesis: C0[i] = sum_l e0_inv[i][l] c[l]
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < m; ++l) acc = fma(__ldg(e0I + i * m + l), c[l], acc);
+          C0[i * B + b] = acc;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ inverse fill
+template <class C>
+__device__ __forceinline__ void inverse_fill(double* R, const double2* __restrict__ mkh,
+                                             const double2* __restrict__ om) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  const double* T = R;  // slot row r sits at tile position m + r
+  double2 z[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    z[i] = make_double2(0.0, 0.0);
+    if (it < ITEMS) {
+      const int job = it % J, tt = it / J;
+      if (tt > 0) {
+        if (job < NPAIR + C::Bm) {
+          const double2 w = __ldg(mkh + tt);
+          double ax, ar, bx, br;  // V1 = w (ax - i ar), V2 = w (bx - i br)
+          if (job < NPAIR) {
+            const int ii = job / B, b = job % B;
+            ax = T[C::ix(m + (tt - 1) * n + 1 + C::ne + ii, b)];
+            ar = T[C::ix(m + (N - tt - 1) * n + 1 + C::ne + ii, b)];
+            bx = T[C::ix(m + (N - tt - 1) * n + 1 + ii, b)];
+            br = T[C::ix(m + (tt - 1) * n + 1 + ii, b)];
+          } else {
+            const int b = job - NPAIR, b2 = b + Bh;
+            ax = T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b)];
+            ar = T[C::ix(m + (tt - 1) * n + 1 + C::half, b)];
+            bx = b2 < B ? T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b2)] : 0.0;
+            br = b2 < B ? T[C::ix(m + (tt - 1) * n + 1 + C::half, b2)] : 0.0;
+          }
+          const double2 v1 = c_mul(w, make_double2(ax, -ar));
+          const double2 v2 = c_mul(w, make_double2(bx, -br));
+          // conj(V1 + i V2): the inverse DFT runs as a forward FFT of the conjugate
+          z[i] = make_double2(v1.x - v2.y, -(v1.y + v2.x));
+        } else {
+          const int jb = job - NPAIR - C::Bm;
+          const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+          z[i] = make_double2(T[C::ix(m + (tt - 1) * n, b)], b2 < B ? T[C::ix(m + (tt - 1) * n, b2)] : 0.0);
+          if (which) z[i] = c_mul(z[i], __ldg(om + tt));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double2* W = reinterpret_cast<double2*>(R);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) W[it] = z[i];
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ inverse post
+template <class C>
+__device__ __forceinline__ void inverse_post(double* R, const double* C0) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  const double2* Z = reinterpret_cast<const double2*>(R);
+  double v1[IPT], v2[IPT];
+  int i1[IPT], i2[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    i1[i] = -1;
+    i2[i] = -1;
+    v1[i] = v2[i] = 0.0;
+    if (it < ITEMS) {
+      const int job = it % J, tt = it / J;
+      if (job < NPAIR + C::Bm) {
+        const double2 u = Z[tt * J + job];
+        const double ure = u.x, uim = -u.y;
+        const int e = makhoul_src(tt, N);
+        const bool odd = e & 1;
+        if (job < NPAIR) {
+          const int ii = job / B, b = job % B;
+          const double o = ure;
+          const double ev = odd ? -uim : uim;
+          const double ci = odd ? -C0[(m - 1 - ii) * B + b] : C0[ii * B + b];
+          const double cr = odd ? -C0[ii * B + b] : C0[(m - 1 - ii) * B + b];
+          v1[i] = ci + ev + o;
+          v2[i] = cr + ev - o;
+          i1[i] = C::ix(e * n + ii, b);
+          i2[i] = C::ix(e * n + m - 1 - ii, b);
+        } else {
+          const int b = job - NPAIR, b2 = b + Bh;
+          constexpr int hc = C::half;
+          const double c1 = odd ? -C0[hc * B + b] : C0[hc * B + b];
+          v1[i] = c1 + (odd ? -ure : ure);
+          i1[i] = C::ix(e * n + hc, b);
+          if (b2 < B) {
+            const double c2 = odd ? -C0[hc * B + b2] : C0[hc * B + b2];
+            v2[i] = c2 + (odd ? -uim : uim);
+            i2[i] = C::ix(e * n + hc, b2);
+          }
+        }
+      } else {
+        const int jb = job - NPAIR - C::Bm;
+        const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+        const int j = tt;
+        if (j >= 1 && j <= N - 1 && (j & 1) == which) {
+          double2 d;
+          if (!which) {
+            const int kp = j / 2;
+            d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
+          } else {
+            const int kp = (j - 1) / 2;
+            d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
+          }
+          v1[i] = 0.5 * d.y;
+          i1[i] = C::ix(j * n - 1, b);
+          if (b2 < B) {
+            v2[i] = -0.5 * d.x;
+            i2[i] = C::ix(j * n - 1, b2);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    if (i1[i] >= 0) R[i1[i]] = v1[i];
+    if (i2[i] >= 0) R[i2[i]] = v2[i];
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ kernel
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+
+template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
+__global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)
+    sweep_mid(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
+              const double* __restrict__ e0F) {
+  using C = Cfg<NN, K, BB, TH, ROWS>;
+  constexpr int B = C::B, L = C::L;
+  extern __shared__ __align__(16) double smem[];
+  double* R = smem;
+  double* C0 = smem + C::C0_OFF;
+  double* PS = smem + C::PS_OFF;
+  double* base = smem + C::BASE_OFF;
+  __shared__ long long off[B];
+  SFEM_PT_DECL;
+  SFEM_PT(0);
+
+  const long long l0 = static_cast<long long>(blockIdx.x) * B;
+  const int Bv = static_cast<int>(min(static_cast<long long>(B), ls.nlines - l0));
+  if (threadIdx.x < B) {
+    const int b = threadIdx.x;
+    const long long l = l0 + b;
+    const long long r = l / ls.ninner;
+    off[b] = l < ls.nlines ? (r / ls.n1) * ls.os2 + (r % ls.n1) * ls.os1 + (l % ls.ninner) * ls.is : 0;
+    if (MODE == kForwardDivideInverse) {
+      // base = shift + sum_{i<N-1} f_i lambda_i (poisson.cpp:586-590 order)
+      long long rem = l < ls.nlines ? l : 0;
+      double terms[kMaxDim];
+#pragma unroll
+      for (int i = kMaxDim - 1; i >= 0; --i) {
+        terms[i] = 0.0;
+        if (i < sym.nlead) {
+          const long long a = rem % sym.lead_ext[i];
+          rem /= sym.lead_ext[i];
+          terms[i] = sym.lead_f[i] * sym.lead_eig[i][a];
+        }
+      }
+      double s = sym.shift;
+#pragma unroll
+      for (int i = 0; i < kMaxDim; ++i)
+        if (i < sym.nlead) s += terms[i];
+      base[b] = s;
+    }
+  }
+  __syncthreads();
+
+  // tile load, all copies in flight at once (phantom lines zero-filled)
+  const long long ps = ls.ps;
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      cp_async8(R + C::ix(pos, b), ls.src + off[b] + pos, b < Bv);
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      cp_async8(R + it, ls.src + off[b] + pos * ps, b < Bv);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  SFEM_PT(1);
+
+  if (MODE != kInverse) {
+    forward_fill<C>(R, PS, t.om);
+    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    centre_reduce<C>(PS, C0);  // PS / C0 are outside the region
+    forward_post<C>(R, t.mk);
+  }
+  SFEM_PT(2);
+  mix<C, MODE>(R, C0, mixF, e0F, t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  SFEM_PT(3);
+  if (MODE != kForward) {
+    inverse_fill<C>(R, t.mkh, t.om);
+    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    inverse_post<C>(R, C0);
+  }
+  SFEM_PT(4);
+
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      if (b < Bv) ls.dst[off[b] + pos] = R[C::ix(pos, b)];
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      if (b < Bv) ls.dst[off[b] + pos * ps] = R[it];
+    }
+  }
+  SFEM_PT(5);
+  SFEM_PT_FLUSH(20 + MODE);
+}
+
+template <int NN, int K, int BB, int TH>
+cudaError_t launch(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
+                   cudaStream_t stream) {
+  const double* mixF = analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w;
+  const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
+  SymbolInfo s{};
+  if (sym) s = *sym;
+  const dim3 grid(static_cast<unsigned>((ls.nlines + BB - 1) / BB));
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto kern, size_t smem) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (err != cudaSuccess) return;
+    kern<<<grid, TH, smem, stream>>>(t, ls, s, mixF, e0F);
+    err = cudaGetLastError();
+  };
+  constexpr size_t SR = Cfg<NN, K, BB, TH, true>::SMEM, SS = Cfg<NN, K, BB, TH, false>::SMEM;
+  if (mode == kForwardDivideInverse) {
+    if (!ls.contiguous) return cudaErrorNotSupported;
+    go(sweep_mid<NN, K, BB, TH, kForwardDivideInverse, true>, SR);
+  } else if (mode == kForward) {
+    if (ls.contiguous)
+      go(sweep_mid<NN, K, BB, TH, kForward, true>, SR);
+    else
+      go(sweep_mid<NN, K, BB, TH, kForward, false>, SS);
+  } else {
+    if (ls.contiguous)
+      go(sweep_mid<NN, K, BB, TH, kInverse, true>, SR);
+    else
+      go(sweep_mid<NN, K, BB, TH, kInverse, false>, SS);
+  }
+  return err;
+}
+
+SFEM_PHASE_EXPORT(sfem_debug_phase_records_mid)
+
+}  // namespace mid
+
+// Threads per CTA for the B = 8 tiles that fit two CTAs per SM.
+#ifndef SFEM_MID_TH256
+#define SFEM_MID_TH256 0
+#endif
+constexpr int kMidTH = SFEM_MID_TH256 ? 256 : 512;
+
+bool has_mid_sweep(int n, int K) {
+  return (n == 1 && K == 1024) || (n == 2 && K == 512) || (n == 4 && K == 256) || (n == 9 && K == 114) ||
+         (n == 9 && K == 1024);
+}
+
+cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
+                             cudaStream_t stream) {
+  if (ls.nlines <= 0) return cudaSuccess;
+  if (t.n == 1 && t.K == 1024) return mid::launch<1, 1024, 8, 512>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 2 && t.K == 512) return mid::launch<2, 512, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 4 && t.K == 256) return mid::launch<4, 256, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 9 && t.K == 114) return mid::launch<9, 114, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 9 && t.K == 1024) return mid::launch<9, 1024, 2, 512>(t, ls, mode, analysis, sym, stream);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace sfem_b200

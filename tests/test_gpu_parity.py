@@ -296,6 +296,35 @@ def test_long_lines_match_oracle(sfem, n, K):
         assert rel_l2(sfem.lines(t, op, x), fn(x, ot)) <= TOL
 
 
+MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024)]
+
+
+@pytest.mark.parametrize("n,K", MID)
+def test_mid_kernels_match_generic_and_oracle(sfem, n, K, monkeypatch):
+    # (n, K) with a sweep_mid.cu specialisation (C5's and C3's line lengths):
+    # 1D ops on a ragged line count, and 2D solves with the specialised axis
+    # strided (axis 0) and contiguous / fused (last axis), against the oracle
+    # and the generic kernels (SFEM_GENERIC=1).
+    t = sfem.SpectralTable(n, K)
+    ot = O.table(n, K)
+    x = np.random.default_rng(K + n).standard_normal((11, n * K - 1))
+    cases = [([n, 2], [K, 5], [1.0, 0.5], 0.5), ([3, n], [4, K], [2.0, 1.0], 0.0)]
+    fs = [np.random.default_rng(i).uniform(-1, 1, [a * b - 1 for a, b in zip(o, e)])
+          for i, (o, e, _, _) in enumerate(cases)]
+    got_lines = [sfem.lines(t, op, x) for op in (0, 1, 2)]
+    got_u = [sfem.solve_dof(sfem.ProblemSpec(2, ln, e, o, sh), f)[0] for (o, e, ln, sh), f in zip(cases, fs)]
+    monkeypatch.setenv("SFEM_GENERIC", "1")
+    gen_lines = [sfem.lines(t, op, x) for op in (0, 1, 2)]
+    gen_u = [sfem.solve_dof(sfem.ProblemSpec(2, ln, e, o, sh), f)[0] for (o, e, ln, sh), f in zip(cases, fs)]
+    monkeypatch.delenv("SFEM_GENERIC")
+    for a, g, fn in zip(got_lines, gen_lines, (O.decompose_weighted, O.decompose, O.synthesize)):
+        assert rel_l2(a, fn(x, ot)) <= TOL
+        assert rel_l2(a, g) <= 1e-13
+    for u, g, (o, e, ln, sh), f in zip(got_u, gen_u, cases, fs):
+        assert rel_l2(u, O.solve_full_diagonalization(f, o, e, ln, sh)) <= TOL
+        assert rel_l2(u, g) <= 1e-13
+
+
 def test_pipelined_host_batch_matches_single_solves(sfem):
     spec = sfem.ProblemSpec(3, [1.0] * 3, [16, 16, 16], [9, 9, 9], 0.5)
     plan = sfem.Plan(spec)

@@ -21,11 +21,12 @@ import torch  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
+ap.add_argument("--fn", default="sfem_debug_phase_records", help="export (…_mid for sweep_mid.cu)")
 a = ap.parse_args()
 orders, elements, lengths, coeffs, shift, _ = bench.CONFIGS[a.config]
 plan = sfem.Plan(sfem.ProblemSpec(len(orders), lengths, elements, orders, shift, coefficients=coeffs))
 d = torch.rand(list(plan.extents[:-1]) + [plan.pitch], dtype=torch.float64, device="cuda")
-fn = sfem.lib.sfem_debug_phase_records
+fn = getattr(sfem.lib, a.fn)
 fn.restype = ctypes.c_longlong
 fn.argtypes = [ctypes.c_void_p, ctypes.c_longlong]
 cap = 1 << 20

@@ -8,7 +8,7 @@ mkdir -p ../variants
 while [ $# -ge 2 ]; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
     -Xcompiler -fPIC,-fopenmp,-O3 $2 -shared -o ../variants/$1.so \
-    csrc/sweep.cu csrc/sweep_fast.cu csrc/dist.cu csrc/capi.cu csrc/table.cpp -lgomp > ../variants/$1.log 2>&1 &
+    csrc/*.cu csrc/*.cpp -lgomp > ../variants/$1.log 2>&1 &
   shift 2
 done
 wait
