@@ -26,7 +26,7 @@ import numpy as np
 __all__ = [
     "Error", "lib", "lib_path", "Context", "SpectralTable", "TableSet", "ProblemSpec", "SolveOptions",
     "SolveReport", "Plan", "GridFunction1D", "CoefficientArray1D", "GridFunctionND", "solve_with_load",
-    "solve_dof", "synthesize", "decompose", "decompose_weighted", "lines", "DECOMPOSE_WEIGHTED",
+    "solve_dof", "synthesize", "decompose", "decompose_weighted", "lines", "lines_device", "DECOMPOSE_WEIGHTED",
     "DECOMPOSE", "SYNTHESIZE", "default_context", "HEADER_SYMBOLS",
 ]
 
@@ -261,6 +261,13 @@ def lines(table: SpectralTable, op: int, x: np.ndarray) -> np.ndarray:
     out = np.empty_like(x)
     _check(lib.sfem_cuda_lines_host(table.handle, op, x.shape[0], _dptr(x), _dptr(out)))
     return out
+
+
+def lines_device(table: SpectralTable, op: int, count: int, d_in: int, in_pitch: int, d_out: int, out_pitch: int,
+                 stream: Optional[int] = None) -> None:
+    """Batched line transform on device pointers (sfem_cuda_lines_device)."""
+    _check(lib.sfem_cuda_lines_device(table.handle, op, count, ctypes.c_void_p(d_in), in_pitch,
+                                      ctypes.c_void_p(d_out), out_pitch, ctypes.c_void_p(stream or 0)))
 
 
 def synthesize(coeffs: CoefficientArray1D, table: SpectralTable) -> GridFunction1D:

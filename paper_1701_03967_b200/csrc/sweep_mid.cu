@@ -24,6 +24,10 @@
 #include "fft_reg.cuh"
 #include "sweep.cuh"
 
+#ifndef SFEM_MID_R16
+#define SFEM_MID_R16 1
+#endif
+
 namespace sfem_b200 {
 namespace mid {
 
@@ -59,31 +63,32 @@ struct Cfg {
 };
 
 // Radix plans (product = K), chosen so that one pass keeps at most ~24
-// complex values per thread in flight.
-template <int K>
+// complex values per thread in flight (FEW: at most 8 jobs per tile, where
+// a radix-16 pass still fits).
+template <int K, bool FEW>
 struct Plan;
-template <>
-struct Plan<1024> {
+template <bool FEW>
+struct Plan<1024, FEW> {
+#if SFEM_MID_R16
+  static constexpr int NP = FEW ? 3 : 4;
+  static constexpr int R[4] = {FEW ? 16 : 8, 8, FEW ? 8 : 4, 4};
+#else
   static constexpr int NP = 4;
   static constexpr int R[4] = {8, 8, 4, 4};
+#endif
 };
-template <>
-struct Plan<512> {
+template <bool FEW>
+struct Plan<512, FEW> {
   static constexpr int NP = 3;
   static constexpr int R[3] = {8, 8, 8};
 };
-template <>
-struct Plan<256> {
-#if SFEM_MID_TH256
-  static constexpr int NP = 3;
-  static constexpr int R[3] = {4, 8, 8};
-#else
+template <bool FEW>
+struct Plan<256, FEW> {
   static constexpr int NP = 2;
   static constexpr int R[2] = {16, 16};
-#endif
 };
-template <>
-struct Plan<114> {
+template <bool FEW>
+struct Plan<114, FEW> {
   static constexpr int NP = 3;
   static constexpr int R[3] = {2, 3, 19};
 };
@@ -163,7 +168,7 @@ __device__ __forceinline__ void fft_pass(double2* W, const double2* __restrict__
 
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
-  using PL = Plan<C::N>;
+  using PL = Plan<C::N, (C::J <= 8)>;
   if constexpr (P < PL::NP) {
     constexpr int R = PL::R[P];
     fft_pass<C, R, NS>(W, tw);
@@ -171,20 +176,45 @@ __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) 
   }
 }
 
+// Item -> (job, index) for the fill / post stages with warps uniform in the
+// job kind: items are grouped pair jobs | middle jobs | nodal jobs, each
+// group index-major with its jobs fastest (consecutive lanes write
+// consecutive W entries of one index: conflict-free).
+template <class C, int NT>
+__device__ __forceinline__ void item_job(int it, int& job, int& t) {
+  constexpr int NP = C::NPAIR, NM = C::Bm, ND = 2 * C::Bh;
+  constexpr int P = NP * NT, PM = (NP + NM) * NT;
+  if (NP > 0 && it < P) {
+    job = it % (NP > 0 ? NP : 1);
+    t = it / (NP > 0 ? NP : 1);
+  } else if (NM > 0 && it < PM) {
+    const int r = it - P;
+    job = NP + r % (NM > 0 ? NM : 1);
+    t = r / (NM > 0 ? NM : 1);
+  } else {
+    const int r = it - PM;
+    job = NP + NM + r % ND;
+    t = r / ND;
+  }
+}
+
 // ------------------------------------------------------------ forward fill
 // W[t][job] from the tile (bridge), plus the chunked centre partial sums.
-template <class C>
-__device__ __forceinline__ void forward_fill(double* R, double* PS, const double2* __restrict__ om) {
+// SEP: the tile T is a separate staging buffer, so W is written directly
+// (no bridge); otherwise T aliases the region R.
+template <class C, bool SEP = false>
+__device__ __forceinline__ void forward_fill(const double* T, double* R, double* PS, const double2* __restrict__ om) {
   constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
   constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
-  const double* T = R;
+  double2* W = reinterpret_cast<double2*>(R);
   double2 z[IPT];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int it = threadIdx.x + i * C::THREADS;
     z[i] = make_double2(0.0, 0.0);
     if (it < ITEMS) {
-      const int job = it % J, tt = it / J;
+      int job, tt;
+      item_job<C, N>(it, job, tt);
       if (job < NPAIR) {
         const int ii = job / B, b = job % B;
         const int e = makhoul_src(tt, N);
@@ -210,6 +240,7 @@ __device__ __forceinline__ void forward_fill(double* R, double* PS, const double
           if (which) z[i] = c_mul(z[i], __ldg(om + tt));
         }
       }
+      if (SEP) W[tt * J + job] = z[i];
     }
   }
   // centre partials: sum (i, b) over elements [c * ECH, (c+1) * ECH)
@@ -223,12 +254,17 @@ __device__ __forceinline__ void forward_fill(double* R, double* PS, const double
       for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ix(e * n + m - 1 - ii, b)] : T[C::ix(e * n + ii, b)];
     }
   }
-  __syncthreads();
-  double2* W = reinterpret_cast<double2*>(R);
+  if (!SEP) {
+    __syncthreads();
 #pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int it = threadIdx.x + i * C::THREADS;
-    if (it < ITEMS) W[it] = z[i];  // it = tt * J + job
+    for (int i = 0; i < IPT; ++i) {
+      const int it = threadIdx.x + i * C::THREADS;
+      if (it < ITEMS) {
+        int job, tt;
+        item_job<C, N>(it, job, tt);
+        W[tt * J + job] = z[i];
+      }
+    }
   }
   if (C::NCEN > 0 && cit < C::CHUNKS * C::NCEN) PS[cit] = part;  // NCEN = 0: no centre (n = 1)
   __syncthreads();
@@ -261,7 +297,9 @@ __device__ __forceinline__ void forward_post(double* R, const double2* __restric
     i2[i] = -1;
     v1[i] = v2[i] = 0.0;
     if (it < ITEMS) {
-      const int job = it % J, k = 1 + it / J;
+      int job, k;
+      item_job<C, N - 1>(it, job, k);
+      k += 1;
       if (job < NPAIR + C::Bm) {
         const double2 zk = Z[k * J + job], zc = Z[(N - k) * J + job];
         const double2 w = __ldg(mk + k);
@@ -316,7 +354,7 @@ __device__ __forceinline__ void forward_post(double* R, const double2* __restric
 //   MODE kForwardDivideInverse u = Mi (Mf v / denom)
 // Items (K-1)*B .. (K-1)*B + B - 1 are the centre blocks of the lines.
 template <class C, int MODE>
-__device__ __forceinline__ void mix(double* T, double* C0, const double* __restrict__ mixF,
+__device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, const double* __restrict__ mixF,
                                     const double* __restrict__ e0F, const double* __restrict__ mixI,
                                     const double* __restrict__ e0I, const double* base,
                                     const double* __restrict__ eig, double f_last) {
@@ -326,9 +364,10 @@ __device__ __forceinline__ void mix(double* T, double* C0, const double* __restr
     if (it < (N - 1) * B) {
       const int k = 1 + it / B, b = it % B;
       double* p = T + C::ix(m + (k - 1) * n, b);
+      const double* pin = Tin + C::ix(m + (k - 1) * n, b);
       double v[n], c[n];
 #pragma unroll
-      for (int s = 0; s < n; ++s) v[s] = p[s * C::PSTR];
+      for (int s = 0; s < n; ++s) v[s] = pin[s * C::PSTR];
       if (MODE != kInverse) {
         const double* M = mixF + static_cast<size_t>(k - 1) * n * n;
 #pragma unroll
@@ -373,7 +412,7 @@ __device__ __forceinline__ void mix(double* T, double* C0, const double* __restr
         }
       } else {
 #pragma unroll
-        for (int l = 0; l < m; ++l) c[l] = T[C::ix(l, b)];
+        for (int l = 0; l < m; ++l) c[l] = Tin[C::ix(l, b)];
       }
       if (MODE == kForward) {
 #pragma unroll
@@ -406,7 +445,8 @@ __device__ __forceinline__ void inverse_fill(double* R, const double2* __restric
     const int it = threadIdx.x + i * C::THREADS;
     z[i] = make_double2(0.0, 0.0);
     if (it < ITEMS) {
-      const int job = it % J, tt = it / J;
+      int job, tt;
+      item_job<C, N>(it, job, tt);
       if (tt > 0) {
         if (job < NPAIR + C::Bm) {
           const double2 w = __ldg(mkh + tt);
@@ -442,7 +482,11 @@ __device__ __forceinline__ void inverse_fill(double* R, const double2* __restric
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int it = threadIdx.x + i * C::THREADS;
-    if (it < ITEMS) W[it] = z[i];
+    if (it < ITEMS) {
+      int job, tt;
+      item_job<C, N>(it, job, tt);
+      W[tt * J + job] = z[i];
+    }
   }
   __syncthreads();
 }
@@ -462,7 +506,8 @@ __device__ __forceinline__ void inverse_post(double* R, const double* C0) {
     i2[i] = -1;
     v1[i] = v2[i] = 0.0;
     if (it < ITEMS) {
-      const int job = it % J, tt = it / J;
+      int job, tt;
+      item_job<C, N>(it, job, tt);
       if (job < NPAIR + C::Bm) {
         const double2 u = Z[tt * J + job];
         const double ure = u.x, uim = -u.y;
@@ -590,13 +635,13 @@ __global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)
   SFEM_PT(1);
 
   if (MODE != kInverse) {
-    forward_fill<C>(R, PS, t.om);
+    forward_fill<C>(R, R, PS, t.om);
     fft<C>(reinterpret_cast<double2*>(R), t.tw);
     centre_reduce<C>(PS, C0);  // PS / C0 are outside the region
     forward_post<C>(R, t.mk);
   }
   SFEM_PT(2);
-  mix<C, MODE>(R, C0, mixF, e0F, t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  mix<C, MODE>(R, R, C0, mixF, e0F, t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
   SFEM_PT(3);
   if (MODE != kForward) {
     inverse_fill<C>(R, t.mkh, t.om);
@@ -620,6 +665,7 @@ __global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)
   SFEM_PT_FLUSH(20 + MODE);
 }
 
+
 template <int NN, int K, int BB, int TH>
 cudaError_t launch(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
                    cudaStream_t stream) {
@@ -635,20 +681,17 @@ cudaError_t launch(const DevTable& t, const LineSet& ls, int mode, int analysis,
     kern<<<grid, TH, smem, stream>>>(t, ls, s, mixF, e0F);
     err = cudaGetLastError();
   };
-  constexpr size_t SR = Cfg<NN, K, BB, TH, true>::SMEM, SS = Cfg<NN, K, BB, TH, false>::SMEM;
+  using CR = Cfg<NN, K, BB, TH, true>;
+  using CS = Cfg<NN, K, BB, TH, false>;
   if (mode == kForwardDivideInverse) {
     if (!ls.contiguous) return cudaErrorNotSupported;
-    go(sweep_mid<NN, K, BB, TH, kForwardDivideInverse, true>, SR);
+    go(sweep_mid<NN, K, BB, TH, kForwardDivideInverse, true>, CR::SMEM);
   } else if (mode == kForward) {
-    if (ls.contiguous)
-      go(sweep_mid<NN, K, BB, TH, kForward, true>, SR);
-    else
-      go(sweep_mid<NN, K, BB, TH, kForward, false>, SS);
+    ls.contiguous ? go(sweep_mid<NN, K, BB, TH, kForward, true>, CR::SMEM)
+                  : go(sweep_mid<NN, K, BB, TH, kForward, false>, CS::SMEM);
   } else {
-    if (ls.contiguous)
-      go(sweep_mid<NN, K, BB, TH, kInverse, true>, SR);
-    else
-      go(sweep_mid<NN, K, BB, TH, kInverse, false>, SS);
+    ls.contiguous ? go(sweep_mid<NN, K, BB, TH, kInverse, true>, CR::SMEM)
+                  : go(sweep_mid<NN, K, BB, TH, kInverse, false>, CS::SMEM);
   }
   return err;
 }
