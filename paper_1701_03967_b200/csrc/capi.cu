@@ -188,6 +188,7 @@ struct Step {
   // TMA description (strided steps): tensor map for the data pointer it was
   // encoded for, re-encoded when the pointer changes.
   bool tma = false;
+  bool bulk_rows = false;  // fused last-axis sweep with per-row bulk copies
   TmaGeom geo{};
   cuuint64_t dims[4] = {1, 1, 1, 1}, strides[3] = {0, 0, 0};
   const double* map_ptr = nullptr;
@@ -345,6 +346,10 @@ Step rows_step(const View& v, int mode) {
   sy.shift = v.shift;
   sy.f_last = v.factors[N - 1];
   s.B = choose_tile(v.tables[N - 1]->dev, ls.nlines, &s.gwork);
+  const DevTable& dt = v.tables[N - 1]->dev;
+  // bulk row copies move L rounded up to even doubles per row
+  s.bulk_rows = v.use_fast && mode == kForwardDivideInverse && has_bulk_rows(dt.n, dt.K) &&
+                (v.pitch * 8) % 16 == 0 && ((dt.L + 1) & ~1) <= v.pitch;
   return s;
 }
 
@@ -358,9 +363,12 @@ void launch_steps(std::vector<Step>& steps, double* data, sfem_ctx ctx, cudaStre
     if (kev) ck(cudaEventRecord((*kev)[i], stream), "event");
     const DevTable& dt = s.table->dev;
     const SymbolInfo* sym = s.mode == kForwardDivideInverse ? &s.sym : nullptr;
-    if (s.tma) {
+    const bool aligned = (reinterpret_cast<unsigned long long>(data) % 16) == 0;
+    if (s.tma && aligned) {
       encode_map(s, data);
       ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
+    } else if (s.bulk_rows && aligned) {
+      ck(launch_sweep_bulk_rows(dt, data, data, s.ls.os1, s.ls.nlines, s.sym, stream), "bulk rows sweep launch");
     } else if (s.use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous)) {
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
     } else if (s.use_fast && has_mid_sweep(dt.n, dt.K)) {

@@ -73,6 +73,11 @@ struct TmaGeom {
 cudaError_t launch_sweep_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
                              cudaStream_t stream);
 bool has_tma_sweep(int n, int K);
+// Fused last-axis sweep with per-row bulk copies (K = 64 specialisations):
+// rows of `pitch` doubles (16-byte aligned rows), src may equal dst.
+bool has_bulk_rows(int n, int K);
+cudaError_t launch_sweep_bulk_rows(const DevTable& t, const double* src, double* dst, long long pitch,
+                                   long long nrows, const SymbolInfo& sym, cudaStream_t stream);
 enum AnalysisKind { kWeighted = 0, kDirect = 1 };
 
 // Shared-memory bytes needed for a tile of B lines of table t (FFT work
