@@ -700,9 +700,12 @@ SFEM_PHASE_EXPORT(sfem_debug_phase_records_mid)
 
 }  // namespace mid
 
+#ifndef SFEM_MID_N1_B4
+#define SFEM_MID_N1_B4 0
+#endif
 // Threads per CTA for the B = 8 tiles that fit two CTAs per SM.
 #ifndef SFEM_MID_TH256
-#define SFEM_MID_TH256 0
+#define SFEM_MID_TH256 1
 #endif
 constexpr int kMidTH = SFEM_MID_TH256 ? 256 : 512;
 
@@ -714,7 +717,11 @@ bool has_mid_sweep(int n, int K) {
 cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
                              cudaStream_t stream) {
   if (ls.nlines <= 0) return cudaSuccess;
+#if SFEM_MID_N1_B4
+  if (t.n == 1 && t.K == 1024) return mid::launch<1, 1024, 4, 256>(t, ls, mode, analysis, sym, stream);
+#else
   if (t.n == 1 && t.K == 1024) return mid::launch<1, 1024, 8, 512>(t, ls, mode, analysis, sym, stream);
+#endif
   if (t.n == 2 && t.K == 512) return mid::launch<2, 512, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
   if (t.n == 4 && t.K == 256) return mid::launch<4, 256, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
   if (t.n == 9 && t.K == 114) return mid::launch<9, 114, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
