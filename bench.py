@@ -272,7 +272,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist-single", action="store_true",
                     help="exercise the slab-decomposed path on one GPU (1-rank NCCL group)")
@@ -370,7 +370,8 @@ def main():
 
     # end to end through the public API: every step copies its load from pinned
     # host memory to the device and its solution back (sfem_cuda_solve_host_batch
-    # pipelines step i's H2D with step i-1's solve and step i-2's D2H)
+    # overlaps step i+1's H2D and step i-1's D2H with step i's solve; the batch
+    # includes the pipeline fill and drain)
     h_load = torch.from_numpy(f).pin_memory()
     h_u = torch.empty_like(h_load).pin_memory()
     plan.solve_host_batch([h_load.data_ptr()], [h_u.data_ptr()])  # warm (allocates the slots)
@@ -386,10 +387,11 @@ def main():
     lp = ctypes.cast(ctypes.c_void_p(h_load.data_ptr()), dp)
     up = ctypes.cast(ctypes.c_void_p(h_u.data_ptr()), dp)
     sec = ctypes.c_double()
-    t0 = time.perf_counter()
-    if sfem.lib.sfem_cuda_solve_host(plan.handle, lp, up, ctypes.byref(sec)) != 0:
-        raise RuntimeError(sfem.lib.sfem_cuda_last_error().decode())
-    lat_s = time.perf_counter() - t0
+    for rep in range(2):  # the first call allocates the plan's staging buffer
+        t0 = time.perf_counter()
+        if sfem.lib.sfem_cuda_solve_host(plan.handle, lp, up, ctypes.byref(sec)) != 0:
+            raise RuntimeError(sfem.lib.sfem_cuda_last_error().decode())
+        lat_s = time.perf_counter() - t0
     e2e = {"value": U * world / e2e_s, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * U, "d2h_bytes_per_step": 8 * U,
            "ms_per_step": e2e_s * 1e3, "steps": n_e2e, "api": "sfem_cuda_solve_host_batch (pinned host buffers)",
            "single_solve_latency_ms": lat_s * 1e3}

@@ -94,8 +94,9 @@ int sfem_cuda_solve_device(sfem_plan plan, double* d_data, long long pitch, void
 int sfem_cuda_solve_host(sfem_plan plan, const double* h_load, double* h_u, double* seconds);
 
 /* Pipelined host solves of `count` independent loads with this plan (e.g.
- * several right-hand sides): problem i's host->device copy overlaps the solve
- * of i-1 and the device->host copy of i-2 (two device slots, three streams).
+ * several right-hand sides): the host->device copy of problem i+1 and the
+ * device->host copy of i-1 run while i is solved (three device slots, three
+ * streams).
  * Pinned host buffers are needed for the copies to overlap. */
 int sfem_cuda_solve_host_batch(sfem_plan plan, long long count, const double* const* h_loads, double* const* h_us);
 

@@ -398,11 +398,13 @@ struct sfem_plan_s {
   std::vector<Step> steps;
   double* dwork = nullptr;
   double* dstage = nullptr;  // dense host-transfer staging
-  // pipelined host solves (sfem_cuda_solve_host_batch): two in-flight slots
-  double* pwork[2] = {nullptr, nullptr};
-  double* pstage[2] = {nullptr, nullptr};
+  // pipelined host solves (sfem_cuda_solve_host_batch): kSlots in-flight
+  // problems, so the H2D of i+1 and the D2H of i-1 run during the solve of i
+  static constexpr int kSlots = 3;
+  double* pwork[kSlots] = {};
+  double* pstage[kSlots] = {};
   cudaStream_t pin = nullptr, pout = nullptr;
-  cudaEvent_t e_in[2] = {nullptr, nullptr}, e_comp[2] = {nullptr, nullptr}, e_out[2] = {nullptr, nullptr};
+  cudaEvent_t e_in[kSlots] = {}, e_comp[kSlots] = {}, e_out[kSlots] = {};
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> kev;
   bool use_fast = true;
@@ -803,7 +805,7 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
     cudaSetDevice(p->ctx->device);
     if (p->dwork) cudaFree(p->dwork);
     if (p->dstage) cudaFree(p->dstage);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < sfem_plan_s::kSlots; ++b) {
       if (p->pwork[b]) cudaFree(p->pwork[b]);
       if (p->pstage[b]) cudaFree(p->pstage[b]);
       if (p->e_in[b]) cudaEventDestroy(p->e_in[b]);
@@ -893,7 +895,7 @@ int sfem_cuda_solve_host_batch(sfem_plan p, long long count, const double* const
     if (!p->pin) {
       ck(cudaStreamCreateWithFlags(&p->pin, cudaStreamNonBlocking), "stream");
       ck(cudaStreamCreateWithFlags(&p->pout, cudaStreamNonBlocking), "stream");
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < sfem_plan_s::kSlots; ++b) {
         ck(cudaMalloc(&p->pwork[b], padded * sizeof(double)), "cudaMalloc(work)");
         ck(cudaMalloc(&p->pstage[b], dense * sizeof(double)), "cudaMalloc(stage)");
         ck(cudaEventCreateWithFlags(&p->e_in[b], cudaEventDisableTiming), "event");
@@ -903,10 +905,10 @@ int sfem_cuda_solve_host_batch(sfem_plan p, long long count, const double* const
       }
     }
     cudaStream_t sc = p->ctx->stream;
-    // problem i uses slot b = i % 2: H2D of i+1 overlaps the solve of i and
-    // the D2H of i-1 (three streams; PCIe moves both directions at once)
+    // problem i uses slot b = i % kSlots: H2D of i+1 and D2H of i-1 overlap the
+    // solve of i (three streams; PCIe moves both directions at once)
     for (long long i = 0; i < count; ++i) {
-      const int b = static_cast<int>(i & 1);
+      const int b = static_cast<int>(i % sfem_plan_s::kSlots);
       ck(cudaStreamWaitEvent(p->pin, p->e_out[b], 0), "wait");
       ck(cudaMemcpyAsync(p->pstage[b], h_loads[i], dense * sizeof(double), cudaMemcpyHostToDevice, p->pin), "H2D");
       ck(cudaEventRecord(p->e_in[b], p->pin), "event");

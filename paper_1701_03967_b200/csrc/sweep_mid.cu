@@ -574,7 +574,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool o
 }
 
 template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
-__global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)
+__global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)  // 256-thread tiles: two CTAs per SM
     sweep_mid(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
               const double* __restrict__ e0F) {
   using C = Cfg<NN, K, BB, TH, ROWS>;
