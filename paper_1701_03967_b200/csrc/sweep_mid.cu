@@ -283,68 +283,90 @@ __device__ __forceinline__ void centre_reduce(const double* PS, double* C0) {
 
 // ------------------------------------------------------------ forward post
 // FFT results -> slots S (at tile positions m + (k-1) n + s), bridge.
+// One post item: up to two slot values and their tile indices (-1: none).
+struct Out2 {
+  double v1, v2;
+  int i1, i2;
+};
+
 template <class C>
-__device__ __forceinline__ void forward_post(double* R, const double2* __restrict__ mk) {
+__device__ __forceinline__ Out2 forward_post_item(const double2* Z, int it, const double2* __restrict__ mk) {
   constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
-  constexpr int ITEMS = (N - 1) * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
-  const double2* Z = reinterpret_cast<const double2*>(R);
-  double v1[IPT], v2[IPT];
-  int i1[IPT], i2[IPT];  // destination indices (-1: none)
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int it = threadIdx.x + i * C::THREADS;
-    i1[i] = -1;
-    i2[i] = -1;
-    v1[i] = v2[i] = 0.0;
-    if (it < ITEMS) {
-      int job, k;
-      item_job<C, N - 1>(it, job, k);
-      k += 1;
-      if (job < NPAIR + C::Bm) {
-        const double2 zk = Z[k * J + job], zc = Z[(N - k) * J + job];
-        const double2 w = __ldg(mk + k);
-        // r1 = Re(mk_k V1), r2 = Re(mk_k V2), V1 = (Z_k + conj Z_{N-k})/2, V2 = (Z_k - conj Z_{N-k})/(2i)
-        const double a1 = 0.5 * (zk.x + zc.x), b1 = 0.5 * (zk.y - zc.y);
-        const double a2 = 0.5 * (zk.y + zc.y), b2 = -0.5 * (zk.x - zc.x);
-        v1[i] = w.x * a1 - w.y * b1;
-        v2[i] = w.x * a2 - w.y * b2;
-        if (job < NPAIR) {
-          const int ii = job / B, b = job % B;
-          i1[i] = C::ix(m + (k - 1) * n + 1 + C::ne + ii, b);  // H_k
-          i2[i] = C::ix(m + (N - k - 1) * n + 1 + ii, b);      // G_{N-k}
-        } else {
-          const int b = job - NPAIR, bb = b + Bh;
-          i1[i] = C::ix(m + (N - k - 1) * n + 1 + C::half, b);
-          if (bb < B) i2[i] = C::ix(m + (N - k - 1) * n + 1 + C::half, bb);
-        }
+  Out2 o{0.0, 0.0, -1, -1};
+  int job, k;
+  item_job<C, N - 1>(it, job, k);
+  k += 1;
+  if (job < NPAIR + C::Bm) {
+    const double2 zk = Z[k * J + job], zc = Z[(N - k) * J + job];
+    const double2 w = __ldg(mk + k);
+    // r1 = Re(mk_k V1), r2 = Re(mk_k V2), V1 = (Z_k + conj Z_{N-k})/2, V2 = (Z_k - conj Z_{N-k})/(2i)
+    const double a1 = 0.5 * (zk.x + zc.x), b1 = 0.5 * (zk.y - zc.y);
+    const double a2 = 0.5 * (zk.y + zc.y), b2 = -0.5 * (zk.x - zc.x);
+    o.v1 = w.x * a1 - w.y * b1;
+    o.v2 = w.x * a2 - w.y * b2;
+    if (job < NPAIR) {
+      const int ii = job / B, b = job % B;
+      o.i1 = C::ix(m + (k - 1) * n + 1 + C::ne + ii, b);  // H_k
+      o.i2 = C::ix(m + (N - k - 1) * n + 1 + ii, b);      // G_{N-k}
+    } else {
+      const int b = job - NPAIR, bb = b + Bh;
+      o.i1 = C::ix(m + (N - k - 1) * n + 1 + C::half, b);
+      if (bb < B) o.i2 = C::ix(m + (N - k - 1) * n + 1 + C::half, bb);
+    }
+  } else {
+    const int jb = job - NPAIR - C::Bm;
+    const int b = jb % Bh, which = jb / Bh, bb = b + Bh;
+    if ((k & 1) == which) {
+      double2 d;
+      if (!which) {
+        const int kp = k / 2;
+        d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
       } else {
-        const int jb = job - NPAIR - C::Bm;
-        const int b = jb % Bh, which = jb / Bh, bb = b + Bh;
-        if ((k & 1) == which) {
-          double2 d;
-          if (!which) {
-            const int kp = k / 2;
-            d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
-          } else {
-            const int kp = (k - 1) / 2;
-            d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
-          }
-          // X = d / (2i)
-          v1[i] = 0.5 * d.y;
-          v2[i] = -0.5 * d.x;
-          i1[i] = C::ix(m + (k - 1) * n, b);
-          if (bb < B) i2[i] = C::ix(m + (k - 1) * n, bb);
-        }
+        const int kp = (k - 1) / 2;
+        d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
       }
+      // X = d / (2i)
+      o.v1 = 0.5 * d.y;
+      o.v2 = -0.5 * d.x;
+      o.i1 = C::ix(m + (k - 1) * n, b);
+      if (bb < B) o.i2 = C::ix(m + (k - 1) * n, bb);
+    }
+  }
+  return o;
+}
+
+// Runs ITEMS items of f into the tile R: bridged (all items loaded, barrier,
+// all stored) when the source aliases R, direct otherwise.
+template <class C, bool SEP, int ITEMS, class F>
+__device__ __forceinline__ void run_out2(double* R, F f) {
+  if constexpr (SEP) {
+    for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+      const Out2 o = f(it);
+      if (o.i1 >= 0) R[o.i1] = o.v1;
+      if (o.i2 >= 0) R[o.i2] = o.v2;
+    }
+  } else {
+    constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+    Out2 o[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int it = threadIdx.x + i * C::THREADS;
+      o[i] = it < ITEMS ? f(it) : Out2{0.0, 0.0, -1, -1};
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      if (o[i].i1 >= 0) R[o[i].i1] = o[i].v1;
+      if (o[i].i2 >= 0) R[o[i].i2] = o[i].v2;
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    if (i1[i] >= 0) R[i1[i]] = v1[i];
-    if (i2[i] >= 0) R[i2[i]] = v2[i];
-  }
-  __syncthreads();
+}
+
+// FFT results -> slots S (at tile positions m + (k-1) n + s).
+template <class C, bool SEP = false>
+__device__ __forceinline__ void forward_post(const double2* Z, double* R, const double2* __restrict__ mk) {
+  run_out2<C, SEP, (C::N - 1) * C::J>(R, [&](int it) { return forward_post_item<C>(Z, it, mk); });
 }
 
 // ------------------------------------------------------------ mixes
@@ -434,137 +456,134 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 
 // ------------------------------------------------------------ inverse fill
 template <class C>
-__device__ __forceinline__ void inverse_fill(double* R, const double2* __restrict__ mkh,
-                                             const double2* __restrict__ om) {
+__device__ __forceinline__ double2 inverse_fill_item(const double* T, int it, int& widx,
+                                                     const double2* __restrict__ mkh, const double2* __restrict__ om) {
   constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
-  constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
-  const double* T = R;  // slot row r sits at tile position m + r
-  double2 z[IPT];
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int it = threadIdx.x + i * C::THREADS;
-    z[i] = make_double2(0.0, 0.0);
-    if (it < ITEMS) {
-      int job, tt;
-      item_job<C, N>(it, job, tt);
-      if (tt > 0) {
-        if (job < NPAIR + C::Bm) {
-          const double2 w = __ldg(mkh + tt);
-          double ax, ar, bx, br;  // V1 = w (ax - i ar), V2 = w (bx - i br)
-          if (job < NPAIR) {
-            const int ii = job / B, b = job % B;
-            ax = T[C::ix(m + (tt - 1) * n + 1 + C::ne + ii, b)];
-            ar = T[C::ix(m + (N - tt - 1) * n + 1 + C::ne + ii, b)];
-            bx = T[C::ix(m + (N - tt - 1) * n + 1 + ii, b)];
-            br = T[C::ix(m + (tt - 1) * n + 1 + ii, b)];
-          } else {
-            const int b = job - NPAIR, b2 = b + Bh;
-            ax = T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b)];
-            ar = T[C::ix(m + (tt - 1) * n + 1 + C::half, b)];
-            bx = b2 < B ? T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b2)] : 0.0;
-            br = b2 < B ? T[C::ix(m + (tt - 1) * n + 1 + C::half, b2)] : 0.0;
-          }
-          const double2 v1 = c_mul(w, make_double2(ax, -ar));
-          const double2 v2 = c_mul(w, make_double2(bx, -br));
-          // conj(V1 + i V2): the inverse DFT runs as a forward FFT of the conjugate
-          z[i] = make_double2(v1.x - v2.y, -(v1.y + v2.x));
-        } else {
-          const int jb = job - NPAIR - C::Bm;
-          const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
-          z[i] = make_double2(T[C::ix(m + (tt - 1) * n, b)], b2 < B ? T[C::ix(m + (tt - 1) * n, b2)] : 0.0);
-          if (which) z[i] = c_mul(z[i], __ldg(om + tt));
-        }
+  double2 z = make_double2(0.0, 0.0);
+  int job, tt;
+  item_job<C, N>(it, job, tt);
+  widx = tt * J + job;
+  if (tt > 0) {
+    if (job < NPAIR + C::Bm) {
+      const double2 w = __ldg(mkh + tt);
+      double ax, ar, bx, br;  // V1 = w (ax - i ar), V2 = w (bx - i br)
+      if (job < NPAIR) {
+        const int ii = job / B, b = job % B;
+        ax = T[C::ix(m + (tt - 1) * n + 1 + C::ne + ii, b)];
+        ar = T[C::ix(m + (N - tt - 1) * n + 1 + C::ne + ii, b)];
+        bx = T[C::ix(m + (N - tt - 1) * n + 1 + ii, b)];
+        br = T[C::ix(m + (tt - 1) * n + 1 + ii, b)];
+      } else {
+        const int b = job - NPAIR, b2 = b + Bh;
+        ax = T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b)];
+        ar = T[C::ix(m + (tt - 1) * n + 1 + C::half, b)];
+        bx = b2 < B ? T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b2)] : 0.0;
+        br = b2 < B ? T[C::ix(m + (tt - 1) * n + 1 + C::half, b2)] : 0.0;
       }
+      const double2 v1 = c_mul(w, make_double2(ax, -ar));
+      const double2 v2 = c_mul(w, make_double2(bx, -br));
+      // conj(V1 + i V2): the inverse DFT runs as a forward FFT of the conjugate
+      z = make_double2(v1.x - v2.y, -(v1.y + v2.x));
+    } else {
+      const int jb = job - NPAIR - C::Bm;
+      const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+      z = make_double2(T[C::ix(m + (tt - 1) * n, b)], b2 < B ? T[C::ix(m + (tt - 1) * n, b2)] : 0.0);
+      if (which) z = c_mul(z, __ldg(om + tt));
     }
   }
-  __syncthreads();
-  double2* W = reinterpret_cast<double2*>(R);
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int it = threadIdx.x + i * C::THREADS;
-    if (it < ITEMS) {
-      int job, tt;
-      item_job<C, N>(it, job, tt);
-      W[tt * J + job] = z[i];
+  return z;
+}
+
+// Slots (tile) -> W; bridged when W aliases the tile.
+template <class C, bool SEP = false>
+__device__ __forceinline__ void inverse_fill(const double* T, double2* W, const double2* __restrict__ mkh,
+                                             const double2* __restrict__ om) {
+  constexpr int ITEMS = C::N * C::J;
+  if constexpr (SEP) {
+    for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+      int widx;
+      const double2 z = inverse_fill_item<C>(T, it, widx, mkh, om);
+      W[widx] = z;
     }
+  } else {
+    constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+    double2 z[IPT];
+    int wi[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int it = threadIdx.x + i * C::THREADS;
+      wi[i] = -1;
+      if (it < ITEMS) z[i] = inverse_fill_item<C>(T, it, wi[i], mkh, om);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+      if (wi[i] >= 0) W[wi[i]] = z[i];
   }
   __syncthreads();
 }
 
 // ------------------------------------------------------------ inverse post
 template <class C>
-__device__ __forceinline__ void inverse_post(double* R, const double* C0) {
+__device__ __forceinline__ Out2 inverse_post_item(const double2* Z, int it, const double* C0) {
   constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
-  constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
-  const double2* Z = reinterpret_cast<const double2*>(R);
-  double v1[IPT], v2[IPT];
-  int i1[IPT], i2[IPT];
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int it = threadIdx.x + i * C::THREADS;
-    i1[i] = -1;
-    i2[i] = -1;
-    v1[i] = v2[i] = 0.0;
-    if (it < ITEMS) {
-      int job, tt;
-      item_job<C, N>(it, job, tt);
-      if (job < NPAIR + C::Bm) {
-        const double2 u = Z[tt * J + job];
-        const double ure = u.x, uim = -u.y;
-        const int e = makhoul_src(tt, N);
-        const bool odd = e & 1;
-        if (job < NPAIR) {
-          const int ii = job / B, b = job % B;
-          const double o = ure;
-          const double ev = odd ? -uim : uim;
-          const double ci = odd ? -C0[(m - 1 - ii) * B + b] : C0[ii * B + b];
-          const double cr = odd ? -C0[ii * B + b] : C0[(m - 1 - ii) * B + b];
-          v1[i] = ci + ev + o;
-          v2[i] = cr + ev - o;
-          i1[i] = C::ix(e * n + ii, b);
-          i2[i] = C::ix(e * n + m - 1 - ii, b);
-        } else {
-          const int b = job - NPAIR, b2 = b + Bh;
-          constexpr int hc = C::half;
-          const double c1 = odd ? -C0[hc * B + b] : C0[hc * B + b];
-          v1[i] = c1 + (odd ? -ure : ure);
-          i1[i] = C::ix(e * n + hc, b);
-          if (b2 < B) {
-            const double c2 = odd ? -C0[hc * B + b2] : C0[hc * B + b2];
-            v2[i] = c2 + (odd ? -uim : uim);
-            i2[i] = C::ix(e * n + hc, b2);
-          }
-        }
+  Out2 o{0.0, 0.0, -1, -1};
+  int job, tt;
+  item_job<C, N>(it, job, tt);
+  if (job < NPAIR + C::Bm) {
+    const double2 u = Z[tt * J + job];
+    const double ure = u.x, uim = -u.y;
+    const int e = makhoul_src(tt, N);
+    const bool odd = e & 1;
+    if (job < NPAIR) {
+      const int ii = job / B, b = job % B;
+      const double ev = odd ? -uim : uim;
+      const double ci = odd ? -C0[(m - 1 - ii) * B + b] : C0[ii * B + b];
+      const double cr = odd ? -C0[ii * B + b] : C0[(m - 1 - ii) * B + b];
+      o.v1 = ci + ev + ure;
+      o.v2 = cr + ev - ure;
+      o.i1 = C::ix(e * n + ii, b);
+      o.i2 = C::ix(e * n + m - 1 - ii, b);
+    } else {
+      const int b = job - NPAIR, b2 = b + Bh;
+      constexpr int hc = C::half;
+      const double c1 = odd ? -C0[hc * B + b] : C0[hc * B + b];
+      o.v1 = c1 + (odd ? -ure : ure);
+      o.i1 = C::ix(e * n + hc, b);
+      if (b2 < B) {
+        const double c2 = odd ? -C0[hc * B + b2] : C0[hc * B + b2];
+        o.v2 = c2 + (odd ? -uim : uim);
+        o.i2 = C::ix(e * n + hc, b2);
+      }
+    }
+  } else {
+    const int jb = job - NPAIR - C::Bm;
+    const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+    const int j = tt;
+    if (j >= 1 && j <= N - 1 && (j & 1) == which) {
+      double2 d;
+      if (!which) {
+        const int kp = j / 2;
+        d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
       } else {
-        const int jb = job - NPAIR - C::Bm;
-        const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
-        const int j = tt;
-        if (j >= 1 && j <= N - 1 && (j & 1) == which) {
-          double2 d;
-          if (!which) {
-            const int kp = j / 2;
-            d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
-          } else {
-            const int kp = (j - 1) / 2;
-            d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
-          }
-          v1[i] = 0.5 * d.y;
-          i1[i] = C::ix(j * n - 1, b);
-          if (b2 < B) {
-            v2[i] = -0.5 * d.x;
-            i2[i] = C::ix(j * n - 1, b2);
-          }
-        }
+        const int kp = (j - 1) / 2;
+        d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
+      }
+      o.v1 = 0.5 * d.y;
+      o.i1 = C::ix(j * n - 1, b);
+      if (b2 < B) {
+        o.v2 = -0.5 * d.x;
+        o.i2 = C::ix(j * n - 1, b2);
       }
     }
   }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    if (i1[i] >= 0) R[i1[i]] = v1[i];
-    if (i2[i] >= 0) R[i2[i]] = v2[i];
-  }
-  __syncthreads();
+  return o;
+}
+
+// FFT results + centre -> the line tile R.
+template <class C, bool SEP = false>
+__device__ __forceinline__ void inverse_post(const double2* Z, double* R, const double* C0) {
+  run_out2<C, SEP, C::N * C::J>(R, [&](int it) { return inverse_post_item<C>(Z, it, C0); });
 }
 
 // ------------------------------------------------------------ kernel
@@ -638,15 +657,15 @@ __global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)  // 256-thread tiles: t
     forward_fill<C>(R, R, PS, t.om);
     fft<C>(reinterpret_cast<double2*>(R), t.tw);
     centre_reduce<C>(PS, C0);  // PS / C0 are outside the region
-    forward_post<C>(R, t.mk);
+    forward_post<C>(reinterpret_cast<const double2*>(R), R, t.mk);
   }
   SFEM_PT(2);
   mix<C, MODE>(R, R, C0, mixF, e0F, t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
   SFEM_PT(3);
   if (MODE != kForward) {
-    inverse_fill<C>(R, t.mkh, t.om);
+    inverse_fill<C>(R, reinterpret_cast<double2*>(R), t.mkh, t.om);
     fft<C>(reinterpret_cast<double2*>(R), t.tw);
-    inverse_post<C>(R, C0);
+    inverse_post<C>(reinterpret_cast<const double2*>(R), R, C0);
   }
   SFEM_PT(4);
 
