@@ -372,7 +372,9 @@ void launch_steps(std::vector<Step>& steps, double* data, sfem_ctx ctx, cudaStre
     } else if (s.use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous)) {
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
     } else if (s.use_fast && has_mid_sweep(dt.n, dt.K)) {
-      ck(launch_sweep_mid(dt, s.ls, s.mode, kWeighted, sym, stream), "mid sweep launch");
+      const size_t wd = mid_work_doubles(dt.n, dt.K, s.ls.nlines);
+      double* gw = wd ? scratch_for(ctx, wd) : nullptr;
+      ck(launch_sweep_mid(dt, s.ls, s.mode, kWeighted, sym, stream, gw), "mid sweep launch");
     } else {
       double* gw = nullptr;
       if (s.gwork) gw = scratch_for(ctx, sweep_work_doubles(dt, s.B) * ((s.ls.nlines + s.B - 1) / s.B));
@@ -721,7 +723,9 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
     if (fast_enabled() && has_fast_sweep(t->dev.n, t->dev.K, mode, 1)) {
       ck(launch_sweep_fast(t->dev, ls, mode, analysis, nullptr, s), "lines launch (fast)");
     } else if (fast_enabled() && has_mid_sweep(t->dev.n, t->dev.K)) {
-      ck(launch_sweep_mid(t->dev, ls, mode, analysis, nullptr, s), "lines launch (mid)");
+      const size_t wd = mid_work_doubles(t->dev.n, t->dev.K, count);
+      double* gw = wd ? scratch_for(t->ctx, wd) : nullptr;
+      ck(launch_sweep_mid(t->dev, ls, mode, analysis, nullptr, s, gw), "lines launch (mid)");
     } else {
       bool gwork = false;
       const int B = choose_tile(t->dev, count, &gwork);

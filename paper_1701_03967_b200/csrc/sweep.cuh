@@ -93,9 +93,12 @@ cudaError_t launch_sweep_fast(const DevTable& t, const LineSet& lines, int mode,
 bool has_fast_sweep(int n, int K, int mode, int contiguous);
 
 // Mid-length line kernels (sweep_mid.cu) for the (n, K) they were compiled for.
+// Lines too long for shared-memory FFT buffers run them in global scratch:
+// mid_work_doubles (0 when none is needed) sizes the `gwork` argument.
 bool has_mid_sweep(int n, int K);
+size_t mid_work_doubles(int n, int K, long long nlines);
 cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& lines, int mode, int analysis,
-                             const SymbolInfo* sym, cudaStream_t stream);
+                             const SymbolInfo* sym, cudaStream_t stream, double* gwork = nullptr);
 
 // Launch one sweep over `lines` with tiles of B lines.
 cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int analysis,

@@ -38,7 +38,7 @@ using namespace reg;
 // ROWS: tile stored line-major T[b][pos] (line pitch LP, odd: conflict-free
 // for lanes over lines), used when lines are rows of the tensor; otherwise
 // position-major T[pos][b] (strided axes, lanes over the 8 adjacent lines).
-template <int NN, int K, int BB, int TH, bool ROWS_>
+template <int NN, int K, int BB, int TH, bool ROWS_, bool GW = false>
 struct Cfg {
   static constexpr int n = NN, m = NN - 1, half = m / 2, ne = NN / 2, N = K, L = NN * K - 1;
   static constexpr bool ROWS = ROWS_;
@@ -51,7 +51,7 @@ struct Cfg {
   static constexpr int THREADS = TH;
   static constexpr int WD = 2 * J * K;  // FFT buffer (doubles)
   static constexpr int TD = (ROWS ? LP : L) * B;  // tile (doubles)
-  static constexpr int REGION = WD > TD ? WD : TD;
+  static constexpr int REGION = (GW || TD > WD) ? TD : WD;  // GW: FFT work in global scratch
   static constexpr int NCEN = m * B;  // centre sums
   static constexpr int CHUNKS = NCEN > 0 ? (TH / NCEN > 0 ? TH / NCEN : 1) : 1;
   static constexpr int ECH = (K + CHUNKS - 1) / CHUNKS;  // elements per chunk
@@ -86,6 +86,11 @@ template <bool FEW>
 struct Plan<256, FEW> {
   static constexpr int NP = 2;
   static constexpr int R[2] = {16, 16};
+};
+template <bool FEW>
+struct Plan<4096, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {16, 16, 16};
 };
 template <bool FEW>
 struct Plan<114, FEW> {
@@ -195,6 +200,42 @@ __device__ __forceinline__ void item_job(int it, int& job, int& t) {
     const int r = it - PM;
     job = NP + NM + r % ND;
     t = r / ND;
+  }
+}
+
+// Out-of-place Stockham passes X -> Y (global-memory work buffers for lines
+// too long for shared memory): one item at a time per thread, no bridge.
+template <class C, int R, int NS>
+__device__ __forceinline__ void fft_pass_oop(const double2* X, double2* Y, const double2* __restrict__ tw) {
+  constexpr int N = C::N, J = C::J, NR = N / R, ITEMS = NR * J;
+  constexpr int TSTEP = N / (NS * R);
+  for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+    const int job = it % J, j = it / J, k = j % NS;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      double2 a = X[(j + q * NR) * J + job];
+      if (NS > 1 && q > 0) a = c_mul(a, __ldg(tw + (q * k * TSTEP) % N));
+      v[q] = a;
+    }
+    dft<R, N>(v, tw);
+    const int outb = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int pp = 0; pp < R; ++pp) Y[(outb + pp * NS) * J + job] = v[pp];
+  }
+  __syncthreads();
+}
+
+// Returns the buffer holding the result.
+template <class C, int P = 0, int NS = 1>
+__device__ __forceinline__ double2* fft_oop(double2* X, double2* Y, const double2* __restrict__ tw) {
+  using PL = Plan<C::N, (C::J <= 8)>;
+  if constexpr (P < PL::NP) {
+    constexpr int R = PL::R[P];
+    fft_pass_oop<C, R, NS>(X, Y, tw);
+    return fft_oop<C, P + 1, NS * R>(Y, X, tw);
+  } else {
+    return X;
   }
 }
 
@@ -685,6 +726,125 @@ __global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)  // 256-thread tiles: t
 }
 
 
+// Lines too long for an FFT buffer in shared memory (C2: n=4, K=4096): the
+// tile stays in shared memory, the J*K complex FFT work of the CTA lives in
+// two slices of a global scratch array (L2-resident while the CTA runs; the
+// slices are discarded from L2 at exit, so they never reach HBM).
+template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
+__global__ void __launch_bounds__(TH, 1)
+    sweep_mid_gw(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
+                 const double* __restrict__ e0F, double* gwork) {
+  using C = Cfg<NN, K, BB, TH, ROWS, true>;
+  constexpr int B = C::B, L = C::L, JK = C::J * C::N;
+  extern __shared__ __align__(16) double smem[];
+  double* R = smem;  // tile and slots (REGION >= TD)
+  double* C0 = smem + C::C0_OFF;
+  double* PS = smem + C::PS_OFF;
+  double* base = smem + C::BASE_OFF;
+  __shared__ long long off[B];
+  double2* W0 = reinterpret_cast<double2*>(gwork) + static_cast<size_t>(blockIdx.x) * 2 * JK;
+  double2* W1 = W0 + JK;
+
+  const long long l0 = static_cast<long long>(blockIdx.x) * B;
+  const int Bv = static_cast<int>(min(static_cast<long long>(B), ls.nlines - l0));
+  if (threadIdx.x < B) {
+    const int b = threadIdx.x;
+    const long long l = l0 + b;
+    const long long r = l / ls.ninner;
+    off[b] = l < ls.nlines ? (r / ls.n1) * ls.os2 + (r % ls.n1) * ls.os1 + (l % ls.ninner) * ls.is : 0;
+    if (MODE == kForwardDivideInverse) {
+      long long rem = l < ls.nlines ? l : 0;
+      double terms[kMaxDim];
+#pragma unroll
+      for (int i = kMaxDim - 1; i >= 0; --i) {
+        terms[i] = 0.0;
+        if (i < sym.nlead) {
+          const long long a = rem % sym.lead_ext[i];
+          rem /= sym.lead_ext[i];
+          terms[i] = sym.lead_f[i] * sym.lead_eig[i][a];
+        }
+      }
+      double sb = sym.shift;
+#pragma unroll
+      for (int i = 0; i < kMaxDim; ++i)
+        if (i < sym.nlead) sb += terms[i];
+      base[b] = sb;
+    }
+  }
+  __syncthreads();
+  const long long ps = ls.ps;
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      cp_async8(R + C::ix(pos, b), ls.src + off[b] + pos, b < Bv);
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      cp_async8(R + it, ls.src + off[b] + pos * ps, b < Bv);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  if (MODE != kInverse) {
+    forward_fill<C, true>(R, reinterpret_cast<double*>(W0), PS, t.om);
+    const double2* Z = fft_oop<C>(W0, W1, t.tw);
+    centre_reduce<C>(PS, C0);
+    forward_post<C, true>(Z, R, t.mk);
+  }
+  mix<C, MODE>(R, R, C0, mixF, e0F, t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  if (MODE != kForward) {
+    inverse_fill<C, true>(R, W0, t.mkh, t.om);
+    const double2* Z = fft_oop<C>(W0, W1, t.tw);
+    inverse_post<C, true>(Z, R, C0);
+  }
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      if (b < Bv) ls.dst[off[b] + pos] = R[C::ix(pos, b)];
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      if (b < Bv) ls.dst[off[b] + pos * ps] = R[it];
+    }
+  }
+  // the work slices are dead: drop them from L2 without write-back
+  char* wb = reinterpret_cast<char*>(W0);
+  for (int i = threadIdx.x; i < (2 * JK * 16) / 128; i += TH)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(wb + static_cast<size_t>(i) * 128) : "memory");
+}
+
+template <int NN, int K, int BB, int TH>
+cudaError_t launch_gw(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
+                      double* gwork, cudaStream_t stream) {
+  const double* mixF = analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w;
+  const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
+  SymbolInfo s{};
+  if (sym) s = *sym;
+  const dim3 grid(static_cast<unsigned>((ls.nlines + BB - 1) / BB));
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto kern, size_t smem) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (err != cudaSuccess) return;
+    kern<<<grid, TH, smem, stream>>>(t, ls, s, mixF, e0F, gwork);
+    err = cudaGetLastError();
+  };
+  // shared memory: the tile only (the FFT buffers are global)
+  constexpr size_t SR = Cfg<NN, K, BB, TH, true, true>::SMEM, SS = Cfg<NN, K, BB, TH, false, true>::SMEM;
+  if (mode == kForwardDivideInverse) {
+    if (!ls.contiguous) return cudaErrorNotSupported;
+    go(sweep_mid_gw<NN, K, BB, TH, kForwardDivideInverse, true>, SR);
+  } else if (mode == kForward) {
+    ls.contiguous ? go(sweep_mid_gw<NN, K, BB, TH, kForward, true>, SR)
+                  : go(sweep_mid_gw<NN, K, BB, TH, kForward, false>, SS);
+  } else {
+    ls.contiguous ? go(sweep_mid_gw<NN, K, BB, TH, kInverse, true>, SR)
+                  : go(sweep_mid_gw<NN, K, BB, TH, kInverse, false>, SS);
+  }
+  return err;
+}
+
 template <int NN, int K, int BB, int TH>
 cudaError_t launch(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
                    cudaStream_t stream) {
@@ -730,12 +890,23 @@ constexpr int kMidTH = SFEM_MID_TH256 ? 256 : 512;
 
 bool has_mid_sweep(int n, int K) {
   return (n == 1 && K == 1024) || (n == 2 && K == 512) || (n == 4 && K == 256) || (n == 9 && K == 114) ||
-         (n == 9 && K == 1024);
+         (n == 9 && K == 1024) || (n == 4 && K == 4096);
+}
+
+size_t mid_work_doubles(int n, int K, long long nlines) {
+  if (n == 4 && K == 4096) {  // B = 1: jobs = 1 pair + 1 middle + 2 nodal
+    return static_cast<size_t>(nlines) * 2 * 2 * 4 * 4096;
+  }
+  return 0;
 }
 
 cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, double* gwork) {
   if (ls.nlines <= 0) return cudaSuccess;
+  if (t.n == 4 && t.K == 4096) {
+    if (!gwork) return cudaErrorInvalidValue;
+    return mid::launch_gw<4, 4096, 1, 512>(t, ls, mode, analysis, sym, gwork, stream);
+  }
 #if SFEM_MID_N1_B4
   if (t.n == 1 && t.K == 1024) return mid::launch<1, 1024, 4, 256>(t, ls, mode, analysis, sym, stream);
 #else

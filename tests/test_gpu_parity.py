@@ -296,7 +296,7 @@ def test_long_lines_match_oracle(sfem, n, K):
         assert rel_l2(sfem.lines(t, op, x), fn(x, ot)) <= TOL
 
 
-MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024)]
+MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024), (4, 4096)]
 
 
 @pytest.mark.parametrize("n,K", MID)
