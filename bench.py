@@ -224,10 +224,11 @@ def run_distributed(args, world, rank, local, dist):
     value = U * args.steps / (ms * 1e-3)
     ms_step = ms / args.steps
     peaks, peak_kind = measured_peaks()
-    # per-rank HBM bytes per solve: 2N-1 sweeps + 2 transposes + 2 2-D copies (read + write each)
+    # per-rank HBM bytes per solve: 2N-1 sweeps + 2 transposes (+ 2 2-D copies
+    # unless the axis-0 sweep runs on the exchange buffer), read + write each
     local_u = U / world
     sweep_bytes = 16.0 * local_u * (2 * len(orders) - 1)
-    copy_bytes = 16.0 * local_u * 4
+    copy_bytes = 16.0 * local_u * (2 if plan.y_elems == 0 else 4)
     achieved = (sweep_bytes + copy_bytes) / (ms_step * 1e-3) / 1e9
     a2a_bytes = 2 * 8.0 * sum(c for i, c in enumerate(plan.send_counts) if i != rank)
 

@@ -368,7 +368,13 @@ void launch_steps(std::vector<Step>& steps, double* data, sfem_ctx ctx, cudaStre
       encode_map(s, data);
       ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
     } else if (s.bulk_rows && aligned) {
-      ck(launch_sweep_bulk_rows(dt, data, data, s.ls.os1, s.ls.nlines, s.sym, stream), "bulk rows sweep launch");
+      RowSegs rs{};
+      rs.n = 1;
+      rs.pos0[0] = 0;
+      rs.len[0] = static_cast<int>((dt.L + 1) & ~1);
+      rs.off[0] = 0;
+      rs.stride[0] = s.ls.os1;
+      ck(launch_sweep_bulk_rows(dt, data, rs, s.ls.nlines, s.sym, stream), "bulk rows sweep launch");
     } else if (s.use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous)) {
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
     } else if (s.use_fast && has_mid_sweep(dt.n, dt.K)) {
@@ -594,14 +600,39 @@ struct sfem_dist_s {
   std::vector<long long> ext;
   std::vector<double> factors;
   double shift = 0;
-  std::vector<long long> x0, lx, y0, ly;
+  std::vector<long long> x0, lx, lxp, y0, ly;  // lxp: lx rounded up to even (exchange block pitch)
   long long R = 1, xpitch = 0, ypitch = 0;
+  bool fused_y = false;  // AXIS0 runs on the exchange buffer in place (no UNPACK1 / PACK2)
+  RowSegs ysegs{};
   View xv, yv;
   std::vector<Step> phaseA, phaseB, phaseC;
   SlabView sv{};
 };
 
 namespace {
+
+// Axis-0 slabs: even sizes (pairs of rows split as evenly as possible), the
+// odd remainder taken off the last non-empty slab, so every slab starts at an
+// even row and every exchange block row (padded to lxp = lx rounded up to
+// even) is a 16-byte multiple at a 16-byte offset.
+std::vector<long long> balanced_even(long long n, int parts, std::vector<long long>& off) {
+  const long long pairs = (n + 1) / 2;
+  std::vector<long long> len(parts);
+  off.assign(parts, 0);
+  long long acc = 0;
+  for (int r = 0; r < parts; ++r) {
+    len[r] = 2 * (pairs / parts + (r < pairs % parts ? 1 : 0));
+    off[r] = acc;
+    acc += len[r];
+  }
+  if (acc > n)
+    for (int r = parts - 1; r >= 0; --r)
+      if (len[r] > 0) {
+        len[r] -= acc - n;
+        break;
+      }
+  return len;
+}
 
 std::vector<long long> balanced(long long n, int parts, std::vector<long long>& off) {
   std::vector<long long> len(parts);
@@ -1007,8 +1038,10 @@ int sfem_cuda_dist_create(sfem_ctx ctx, int dim, const int* orders, const int* e
       d->ext.push_back(static_cast<long long>(orders[i]) * elements[i] - 1);
     }
     require(d->ext[0] >= nranks && d->ext[1] >= nranks, "dist_create: fewer slab rows than ranks");
-    d->lx = balanced(d->ext[0], nranks, d->x0);
+    d->lx = balanced_even(d->ext[0], nranks, d->x0);
     d->ly = balanced(d->ext[1], nranks, d->y0);
+    d->lxp.resize(nranks);
+    for (int p = 0; p < nranks; ++p) d->lxp[p] = d->lx[p] + (d->lx[p] & 1);
     for (int i = 2; i < dim; ++i) d->R *= d->ext[i];
     d->xpitch = (d->ext[dim - 1] + 3) & ~3LL;
     d->ypitch = (d->ext[0] + 3) & ~3LL;
@@ -1051,12 +1084,34 @@ int sfem_cuda_dist_create(sfem_ctx ctx, int dim, const int* orders, const int* e
       for (int a = 1; a <= dim - 2; ++a) d->phaseC.push_back(strided_step(xv, a, kInverse));
       d->phaseC.push_back(rows_step(xv, kInverse));
     }
-    // phase B: fused forward + divide + inverse along axis 0 on the y-slab
+    // phase B: fused forward + divide + inverse along axis 0 on the y-slab, or
+    // (K = 64 tables) straight on the source-major blocks of the exchange
+    // buffer: row q of the y-slab is the concatenation over sources p of
+    // buf[lyR * x0_p + q * lxp_p + (0 .. lxp_p)]
     if (yv.ext[0] > 0) d->phaseB.push_back(rows_step(yv, kForwardDivideInverse));
+    {
+      const long long lyR = d->ly[rank] * d->R;
+      const DevTable& t0 = d->tables[0]->dev;
+      d->fused_y = fast && nranks <= kMaxSeg && has_bulk_rows(t0.n, t0.K) && lyR > 0 && !d->phaseB.empty() &&
+                   d->phaseB[0].bulk_rows;
+      if (d->fused_y) {
+        RowSegs& rs = d->ysegs;
+        rs.n = 0;
+        for (int p = 0; p < nranks; ++p) {
+          if (d->lx[p] == 0) continue;
+          rs.pos0[rs.n] = static_cast<int>(d->x0[p]);
+          rs.len[rs.n] = static_cast<int>(d->lxp[p]);
+          rs.off[rs.n] = lyR * d->x0[p];
+          rs.stride[rs.n] = d->lxp[p];
+          ++rs.n;
+        }
+      }
+    }
     // transpose view of the x-slab
     const std::vector<long long> st = xv.strides();
     SlabView& sv = d->sv;
     sv.lx = d->lx[rank];
+    sv.bpitch = d->lxp[rank];
     sv.R = d->R;
     sv.Q = d->ext[1] * d->R;
     sv.st0 = st[0];
@@ -1088,11 +1143,11 @@ int sfem_cuda_dist_shape(sfem_dist d, long long* info, long long* send_counts, l
     info[2] = d->y0[r];
     info[3] = d->ly[r];
     info[4] = d->xv.rows() * d->xpitch;  // x-slab elements (padded)
-    info[5] = d->ly[r] * d->R * d->ypitch;  // y-slab elements
+    info[5] = d->fused_y ? 0 : d->ly[r] * d->R * d->ypitch;  // y-slab elements (unused when fused)
     long long sx = 0, rx = 0;
     for (int p = 0; p < d->nranks; ++p) {
-      const long long sc = d->lx[r] * d->ly[p] * d->R;  // exchange 1: to p
-      const long long rc = d->lx[p] * d->ly[r] * d->R;  // exchange 1: from p
+      const long long sc = d->lxp[r] * d->ly[p] * d->R;  // exchange 1: to p (blocks [ly_p R][lxp_r])
+      const long long rc = d->lxp[p] * d->ly[r] * d->R;  // exchange 1: from p
       if (send_counts) send_counts[p] = sc;
       if (recv_counts) recv_counts[p] = rc;
       sx += sc;
@@ -1119,22 +1174,29 @@ int sfem_cuda_dist_phase(sfem_dist d, int phase, double* x, double* y, double* b
       case SFEM_DIST_PACK1:  // x-slab -> [L1*R][lx] (destination-major blocks)
         ck(launch_slab_transpose(d->sv, x, buf, true, s), "slab transpose");
         break;
-      case SFEM_DIST_UNPACK1:  // blocks [ly*R][lx_p] from each source p -> y rows, columns x0_p..
+      case SFEM_DIST_UNPACK1:  // blocks [ly*R][lxp_p] from each source p -> y rows, columns x0_p..
+        if (d->fused_y) break;
         for (int p = 0; p < d->nranks; ++p) {
           if (d->lx[p] == 0 || lyR == 0) continue;
           ck(cudaMemcpy2DAsync(y + d->x0[p], d->ypitch * sizeof(double), buf + lyR * d->x0[p],
-                               d->lx[p] * sizeof(double), d->lx[p] * sizeof(double), lyR,
+                               d->lxp[p] * sizeof(double), d->lx[p] * sizeof(double), lyR,
                                cudaMemcpyDeviceToDevice, s),
              "unpack1");
         }
         break;
       case SFEM_DIST_AXIS0:
-        launch_steps(d->phaseB, y, d->ctx, s, nullptr);
+        if (d->fused_y) {
+          const Step& st = d->phaseB[0];
+          ck(launch_sweep_bulk_rows(st.table->dev, buf, d->ysegs, lyR, st.sym, s), "axis0 (exchange buffer)");
+        } else {
+          launch_steps(d->phaseB, y, d->ctx, s, nullptr);
+        }
         break;
-      case SFEM_DIST_PACK2:  // y rows, columns x0_p.. -> blocks [ly*R][lx_p] for each destination p
+      case SFEM_DIST_PACK2:  // y rows, columns x0_p.. -> blocks [ly*R][lxp_p] for each destination p
+        if (d->fused_y) break;
         for (int p = 0; p < d->nranks; ++p) {
           if (d->lx[p] == 0 || lyR == 0) continue;
-          ck(cudaMemcpy2DAsync(buf + lyR * d->x0[p], d->lx[p] * sizeof(double), y + d->x0[p],
+          ck(cudaMemcpy2DAsync(buf + lyR * d->x0[p], d->lxp[p] * sizeof(double), y + d->x0[p],
                                d->ypitch * sizeof(double), d->lx[p] * sizeof(double), lyR,
                                cudaMemcpyDeviceToDevice, s),
              "pack2");

@@ -8,6 +8,7 @@ namespace sfem_b200 {
 // x-slab [lx][L1][rest] viewed as (a0l, q) with q = a1 * R + r.
 struct SlabView {
   long long lx;   // local rows of axis 0
+  long long bpitch;  // exchange-buffer row pitch (lx rounded up to even; pad column written as 0)
   long long Q;    // L1 * R
   long long R;    // product of the rest extents (1 for N = 2)
   long long st0;  // x stride of axis 0 (elements)

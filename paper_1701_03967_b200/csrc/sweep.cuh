@@ -73,11 +73,22 @@ struct TmaGeom {
 cudaError_t launch_sweep_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
                              cudaStream_t stream);
 bool has_tma_sweep(int n, int K);
-// Fused last-axis sweep with per-row bulk copies (K = 64 specialisations):
-// rows of `pitch` doubles (16-byte aligned rows), src may equal dst.
+// Fused last-axis sweep with per-row bulk copies (K = 64 specialisations).
+// A row is the concatenation of `n` segments: segment s of row q holds
+// positions [pos0[s], pos0[s] + len[s]) at base + off[s] + q * stride[s]
+// (elements; every offset, stride and length even so the copies are 16-byte
+// aligned).  One segment (off 0, stride = pitch, len = L rounded up to even)
+// is a plain dof tensor; the multi-GPU axis-0 sweep reads and writes the
+// source-major blocks of the exchange buffer directly.  In place.
+constexpr int kMaxSeg = 8;
+struct RowSegs {
+  int n;
+  int pos0[kMaxSeg], len[kMaxSeg];
+  long long off[kMaxSeg], stride[kMaxSeg];
+};
 bool has_bulk_rows(int n, int K);
-cudaError_t launch_sweep_bulk_rows(const DevTable& t, const double* src, double* dst, long long pitch,
-                                   long long nrows, const SymbolInfo& sym, cudaStream_t stream);
+cudaError_t launch_sweep_bulk_rows(const DevTable& t, double* data, const RowSegs& segs, long long nrows,
+                                   const SymbolInfo& sym, cudaStream_t stream);
 enum AnalysisKind { kWeighted = 0, kDirect = 1 };
 
 // Shared-memory bytes needed for a tile of B lines of table t (FFT work

@@ -5,7 +5,9 @@ The data path per solve on rank r:
     FORWARD_LOCAL(x) -> PACK1 -> all_to_all -> UNPACK1 -> AXIS0(y)
     -> PACK2 -> all_to_all (reverse counts) -> UNPACK2 -> INVERSE_LOCAL(x)
 x = the rank's axis-0 slab of the global dof tensor, y = its axis-1 slab with
-axis 0 contiguous.  The two all-to-alls are the only collectives (NCCL through
+axis 0 contiguous.  With K = 64 tables on the swept axis 0, AXIS0 runs in
+place on the received exchange buffer (each y row is read and written as
+per-source segments) and UNPACK1 / PACK2 are no-ops.  The two all-to-alls are the only collectives (NCCL through
 torch.distributed on GPUs); everything else is the rank's own kernels.
 
 `partition` / `slab_*` restate the C++ slab arithmetic for the host side and
@@ -34,6 +36,26 @@ def partition(n: int, parts: int):
     return offs, lens
 
 
+def partition_even(n: int, parts: int):
+    """Axis-0 split (capi.cu `balanced_even`): pairs of rows balanced, the odd
+    remainder taken off the last non-empty slab, so every slab starts at an
+    even row.  Returns (offsets, lengths)."""
+    pairs = (n + 1) // 2
+    lens = [2 * (pairs // parts + (1 if r < pairs % parts else 0)) for r in range(parts)]
+    extra = sum(lens) - n
+    for r in range(parts - 1, -1, -1):
+        if extra and lens[r] > 0:
+            lens[r] -= extra
+            break
+    offs = [sum(lens[:r]) for r in range(parts)]
+    return offs, lens
+
+
+def padded(lx: int) -> int:
+    """Exchange-buffer block pitch of a slab of lx rows (lx rounded up to even)."""
+    return lx + (lx & 1)
+
+
 @dataclass
 class SlabShape:
     extents: List[int]
@@ -45,7 +67,7 @@ class SlabShape:
         return int(np.prod(self.extents[2:])) if len(self.extents) > 2 else 1
 
     def x(self):
-        offs, lens = partition(self.extents[0], self.nranks)
+        offs, lens = partition_even(self.extents[0], self.nranks)
         return offs[self.rank], lens[self.rank]
 
     def y(self):
@@ -55,12 +77,12 @@ class SlabShape:
     def send_counts1(self) -> List[int]:
         _, lx = self.x()
         _, lys = partition(self.extents[1], self.nranks)
-        return [lx * ly * self.R for ly in lys]
+        return [padded(lx) * ly * self.R for ly in lys]
 
     def recv_counts1(self) -> List[int]:
         _, ly = self.y()
-        _, lxs = partition(self.extents[0], self.nranks)
-        return [lx * ly * self.R for lx in lxs]
+        _, lxs = partition_even(self.extents[0], self.nranks)
+        return [padded(lx) * ly * self.R for lx in lxs]
 
 
 class DistPlan:

@@ -32,14 +32,15 @@ class OracleRank:
     csrc/capi.cu (sfem_cuda_dist_phase) with the numpy oracle transforms."""
 
     def __init__(self, orders, elements, lengths, shift, nranks, rank):
-        from paper_1701_03967_b200.dist import SlabShape, partition
+        from paper_1701_03967_b200.dist import SlabShape, padded, partition_even
         self.orders, self.elements, self.lengths, self.shift = orders, elements, lengths, shift
         self.ext = [n * K - 1 for n, K in zip(orders, elements)]
         self.N = len(orders)
         self.shape = SlabShape(self.ext, nranks, rank)
         self.x0, self.lx = self.shape.x()
         self.y0, self.ly = self.shape.y()
-        self.xoffs, self.xlens = partition(self.ext[0], nranks)
+        self.xoffs, self.xlens = partition_even(self.ext[0], nranks)
+        self.lxp = padded(self.lx)
         self.R = self.shape.R
         self.send_counts = self.shape.send_counts1()
         self.recv_counts = self.shape.recv_counts1()
@@ -54,14 +55,17 @@ class OracleRank:
             x = self._along(x, a, O.decompose_weighted, self.tabs[a])
         return x
 
-    def pack1(self, x):  # [lx][L1*R] -> [L1*R][lx]
-        return np.ascontiguousarray(x.reshape(self.lx, -1).T).reshape(-1)
+    def pack1(self, x):  # [lx][L1*R] -> [L1*R][lxp] (pad column zero)
+        t = np.zeros((x.reshape(self.lx, -1).shape[1], self.lxp))
+        t[:, :self.lx] = x.reshape(self.lx, -1).T
+        return t.reshape(-1)
 
-    def unpack1(self, buf):  # blocks [ly*R][lx_p] -> y[ly*R][L0]
+    def unpack1(self, buf):  # blocks [ly*R][lxp_p] -> y[ly*R][L0]
+        from paper_1701_03967_b200.dist import padded
         lyR = self.ly * self.R
         y = np.zeros((lyR, self.ext[0]))
         for p, (o, n) in enumerate(zip(self.xoffs, self.xlens)):
-            y[:, o:o + n] = buf[lyR * o: lyR * (o + n)].reshape(lyR, n)
+            y[:, o:o + n] = buf[lyR * o: lyR * (o + padded(n))].reshape(lyR, padded(n))[:, :n]
         return y
 
     def axis0(self, y):
@@ -78,14 +82,18 @@ class OracleRank:
         return O.synthesize(c / denom, t0)
 
     def pack2(self, y):
+        from paper_1701_03967_b200.dist import padded
         lyR = self.ly * self.R
-        buf = np.zeros(lyR * self.ext[0])
+        buf = np.zeros(lyR * sum(padded(n) for n in self.xlens))
         for o, n in zip(self.xoffs, self.xlens):
-            buf[lyR * o: lyR * (o + n)] = y[:, o:o + n].reshape(-1)
+            blk = np.zeros((lyR, padded(n)))
+            blk[:, :n] = y[:, o:o + n]
+            buf[lyR * o: lyR * (o + padded(n))] = blk.reshape(-1)
         return buf
 
     def unpack2(self, buf):
-        return np.ascontiguousarray(buf.reshape(-1, self.lx).T).reshape([self.lx] + self.ext[1:])
+        t = buf.reshape(-1, self.lxp)[:, :self.lx]
+        return np.ascontiguousarray(t.T).reshape([self.lx] + self.ext[1:])
 
     def inverse_local(self, x):
         for a in range(1, self.N):
@@ -133,17 +141,23 @@ def test_gloo_slab_solve_matches_single_process(tmp_path, world, cfg):
 
 
 def test_partition_and_counts_are_consistent():
-    from paper_1701_03967_b200.dist import SlabShape, partition
+    from paper_1701_03967_b200.dist import SlabShape, padded, partition, partition_even
     for n, P in ((575, 8), (7, 3), (9, 9), (1025, 4)):
         offs, lens = partition(n, P)
         assert sum(lens) == n and offs[0] == 0 and max(lens) - min(lens) <= 1
+    for n, P in ((575, 8), (127, 3), (9, 4), (1025, 4), (16, 8), (15, 8)):
+        offs, lens = partition_even(n, P)
+        assert sum(lens) == n and offs[0] == 0
+        assert all(o % 2 == 0 for o in offs)  # every slab starts at an even row
+        assert sum(1 for ln in lens if ln % 2) <= 1 and max(lens) - min(lens) <= 3
     ext = [575, 575, 575]
     shapes = [SlabShape(ext, 8, r) for r in range(8)]
     # what r sends to s equals what s receives from r
     for r in range(8):
         for s in range(8):
             assert shapes[r].send_counts1()[s] == shapes[s].recv_counts1()[r]
-    assert sum(sum(sh.send_counts1()) for sh in shapes) == int(np.prod(ext))
+    lxs = partition_even(575, 8)[1]
+    assert sum(sum(sh.send_counts1()) for sh in shapes) == sum(padded(lx) for lx in lxs) * 575 * 575
 
 
 @pytest.mark.gpu
@@ -152,6 +166,8 @@ def test_partition_and_counts_are_consistent():
     (2, [2, 3, 2], [8, 5, 9], [1.0, 2.0, 1.0], 0.5),
     (3, [9, 9, 9], [4, 4, 4], [1.0] * 3, 0.0),
     (4, [9, 9], [64, 64], [1.0, 1.0], 1.0),
+    (3, [2, 3], [64, 5], [1.0, 0.5], 0.25),
+    (5, [3, 2, 4], [64, 3, 6], [1.0, 1.0, 2.0], 0.0),
     (8, [9, 9, 9], [64, 64, 64], [1.0] * 3, 0.0),
 ])
 def test_loopback_slab_solve_matches_single_gpu(sfem, P, orders, elements, lengths, shift):
