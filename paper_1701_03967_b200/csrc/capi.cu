@@ -348,8 +348,7 @@ Step rows_step(const View& v, int mode) {
   s.B = choose_tile(v.tables[N - 1]->dev, ls.nlines, &s.gwork);
   const DevTable& dt = v.tables[N - 1]->dev;
   // bulk row copies move L rounded up to even doubles per row
-  s.bulk_rows = v.use_fast && mode == kForwardDivideInverse && has_bulk_rows(dt.n, dt.K) &&
-                (v.pitch * 8) % 16 == 0 && ((dt.L + 1) & ~1) <= v.pitch;
+  s.bulk_rows = v.use_fast && has_bulk_rows(dt.n, dt.K) && (v.pitch * 8) % 16 == 0 && ((dt.L + 1) & ~1) <= v.pitch;
   return s;
 }
 
@@ -374,7 +373,7 @@ void launch_steps(std::vector<Step>& steps, double* data, sfem_ctx ctx, cudaStre
       rs.len[0] = static_cast<int>((dt.L + 1) & ~1);
       rs.off[0] = 0;
       rs.stride[0] = s.ls.os1;
-      ck(launch_sweep_bulk_rows(dt, data, rs, s.ls.nlines, s.sym, stream), "bulk rows sweep launch");
+      ck(launch_sweep_bulk_rows(dt, data, rs, s.ls.nlines, s.mode, kWeighted, s.sym, stream), "bulk rows sweep launch");
     } else if (s.use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous)) {
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
     } else if (s.use_fast && has_mid_sweep(dt.n, dt.K)) {
@@ -1187,7 +1186,8 @@ int sfem_cuda_dist_phase(sfem_dist d, int phase, double* x, double* y, double* b
       case SFEM_DIST_AXIS0:
         if (d->fused_y) {
           const Step& st = d->phaseB[0];
-          ck(launch_sweep_bulk_rows(st.table->dev, buf, d->ysegs, lyR, st.sym, s), "axis0 (exchange buffer)");
+          ck(launch_sweep_bulk_rows(st.table->dev, buf, d->ysegs, lyR, kForwardDivideInverse, kWeighted, st.sym, s),
+             "axis0 (exchange buffer)");
         } else {
           launch_steps(d->phaseB, y, d->ctx, s, nullptr);
         }

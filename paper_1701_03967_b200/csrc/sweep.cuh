@@ -79,7 +79,8 @@ bool has_tma_sweep(int n, int K);
 // (elements; every offset, stride and length even so the copies are 16-byte
 // aligned).  One segment (off 0, stride = pitch, len = L rounded up to even)
 // is a plain dof tensor; the multi-GPU axis-0 sweep reads and writes the
-// source-major blocks of the exchange buffer directly.  In place.
+// source-major blocks of the exchange buffer directly.  In place.  `mode`:
+// kForward / kInverse / kForwardDivideInverse (sym used by the latter only).
 constexpr int kMaxSeg = 8;
 struct RowSegs {
   int n;
@@ -87,8 +88,8 @@ struct RowSegs {
   long long off[kMaxSeg], stride[kMaxSeg];
 };
 bool has_bulk_rows(int n, int K);
-cudaError_t launch_sweep_bulk_rows(const DevTable& t, double* data, const RowSegs& segs, long long nrows,
-                                   const SymbolInfo& sym, cudaStream_t stream);
+cudaError_t launch_sweep_bulk_rows(const DevTable& t, double* data, const RowSegs& segs, long long nrows, int mode,
+                                   int analysis, const SymbolInfo& sym, cudaStream_t stream);
 enum AnalysisKind { kWeighted = 0, kDirect = 1 };
 
 // Shared-memory bytes needed for a tile of B lines of table t (FFT work
