@@ -114,7 +114,7 @@ void upload_table(sfem_table_s* t) {
   std::vector<const std::vector<double>*> parts = {&d.mix_fwd_w, &d.mix_fwd_d, &d.mix_inv, &d.e0_fwd_w,
                                                    &d.e0_fwd_d,  &d.e0_inv,    &d.eig,     &d.tw,
                                                    &d.mk,        &d.mkh,       &d.om,
-                                                   &d.mixT_w,    &d.mixT_d,    &d.mixT_i};
+                                                   &d.mixT_w,    &d.mixT_d,    &d.mixT_i,    &d.nsq};
   std::vector<size_t> offs;
   size_t total = 0;
   for (const auto* p : parts) {
@@ -148,6 +148,7 @@ void upload_table(sfem_table_s* t) {
   v.mixT_w = t->dbuf + offs[11];
   v.mixT_d = t->dbuf + offs[12];
   v.mixT_i = t->dbuf + offs[13];
+  v.nsq = t->dbuf + offs[14];
   const std::vector<int> r = factor_radices(d.K);
   require(static_cast<int>(r.size()) <= kMaxPasses, "table: too many FFT passes");
   v.npass = static_cast<int>(r.size());

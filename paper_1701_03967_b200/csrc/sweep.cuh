@@ -19,6 +19,7 @@ struct DevTable {
   const double* e0_fwd_d;
   const double* e0_inv;
   const double* eig;        // L, coefficient order
+  const double* nsq;        // L, norm_sq in coefficient order (1 for k = 0)
   const double* mixT_w;     // n x n x K, [l][s][k] (k-contiguous copies of mix_fwd_w; k = 0 unused)
   const double* mixT_d;     // same for mix_fwd_d
   const double* mixT_i;     // n x n x K, [s][l][k] copy of mix_inv

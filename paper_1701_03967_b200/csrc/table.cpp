@@ -677,6 +677,13 @@ DeviceTableData derive_device_data(const HostTable& t) {
       d.e0_fwd_d[static_cast<size_t>(i) * m + l] = ce / K;
     }
   d.eig = t.eig_coeff;
+  // norm_sq in coefficient order: the fused last-axis sweep runs the forward
+  // mix with the synthesis matrix (mix_fwd_w[k][l][s] = mix_inv[k][s][l] /
+  // norm_sq[k][l], exactly as formed above) and folds 1/norm_sq into the
+  // symbol divide, so one matrix per frequency serves both mixes.
+  d.nsq.assign(static_cast<size_t>(n) * K - 1, 1.0);
+  for (int k = 1; k < K; ++k)
+    for (int l = 0; l < n; ++l) d.nsq[m + static_cast<size_t>(k - 1) * n + l] = t.norm_sq[static_cast<size_t>(k - 1) * n + l];
   d.mixT_w.assign(nn * K, 0.0);
   d.mixT_d.assign(nn * K, 0.0);
   d.mixT_i.assign(nn * K, 0.0);

@@ -48,6 +48,7 @@ struct DeviceTableData {
   std::vector<double> e0_fwd_d;    // m x m [j][l] = (C~ e^(l))_j / K
   std::vector<double> e0_inv;      // m x m [i][l] = e_i^(l)
   std::vector<double> eig;         // n*K-1
+  std::vector<double> nsq;         // n*K-1: ||s_k^(l)||^2 in coefficient order (1 in the k = 0 block)
   std::vector<double> mixT_w, mixT_d, mixT_i;  // n x n x K, k-contiguous (see sweep.cuh)
   std::vector<double> tw;          // 2N: exp(-2 pi i t/N)   (re, im interleaved)
   std::vector<double> mk;          // 2N: exp(-i pi k/(2N))
