@@ -113,6 +113,37 @@ int sfem_cuda_solve_classes(sfem_plan plan, const double* const* h_load_classes,
 int sfem_cuda_solve_device_timed(sfem_plan plan, double* d_data, long long pitch, int reps, double* total_ms,
                                  double* kernel_ms);
 
+/* ---- The steps either side of the solve, on the device ----
+ * Built-in right-hand sides (the reference's ScalarField callbacks cannot
+ * cross to the device; these are its manufactured cases, cases.cpp:11-55,
+ * plus the product of sines of BASELINE config 3):
+ *   SFEM_FIELD_CONSTANT   f = params[0]                       (cases "constantNd": 1)
+ *   SFEM_FIELD_SINES      f = params[0] * prod_i sin(params[1+i] * pi * x_i);
+ *                         exact u = f / (sum_i a_i (params[1+i] pi)^2 + shift)
+ *   SFEM_FIELD_SIN1D / _POISSON2D / _POISSON3D
+ *                         f = -Lap u + shift u for the reference's u (unit
+ *                         coefficients only, as make_problem, cases.cpp:81-95) */
+enum {
+  SFEM_FIELD_CONSTANT = 0, SFEM_FIELD_SINES = 1, SFEM_FIELD_SIN1D = 2, SFEM_FIELD_POISSON2D = 3,
+  SFEM_FIELD_POISSON3D = 4
+};
+/* FEM load of a field on the plan's box into d_load (dof layout, pitch):
+ * replaces fem_load_average (poisson.cpp:471-569; (n+1)-point Gauss rule per
+ * axis, boundary contributions dropped).  Deterministic (no atomics). */
+int sfem_cuda_fem_load(sfem_plan plan, int field, const double* params, int nparams, double* d_load,
+                       long long pitch, void* stream);
+/* d_y = A d_v, A the plan's FEM operator sum_i f_i (x)_{j!=i} M_j (x) S_i +
+ * shift (x) M_j; replaces apply_operator (poisson.cpp:749-769).  v != y. */
+int sfem_cuda_apply_operator(sfem_plan plan, const double* d_v, double* d_y, long long pitch, void* stream);
+/* residual_rel = max|A u - f| / max|f| (1 if f == 0 everywhere) on the device,
+ * as SolveReport::residual_rel (poisson.cpp:785-789).  Synchronous. */
+int sfem_cuda_residual(sfem_plan plan, const double* d_u, const double* d_f, long long pitch, double* residual_rel);
+/* error = max over the dofs of |u - u_exact| for a field with a known solution
+ * (SINES and the cases); replaces max_error_vs (ndgrid.cpp:80-101; boundary
+ * slots, where u = 0 = u_exact, are not stored).  Synchronous. */
+int sfem_cuda_max_error(sfem_plan plan, int field, const double* params, int nparams, const double* d_u,
+                        long long pitch, double* error);
+
 /* ---- Multi-GPU slab decomposition (one process / context per GPU) ----
  * Rank r owns the x-slab of axis-0 dof rows [x0, x0+lx) of the global dof
  * tensor (all other axes; last axis padded to xpitch) and, between the two

@@ -25,6 +25,7 @@
 #endif
 
 #include "sfem/banded.hpp"
+#include "sfem/cases.hpp"
 #include "sfem/eigenbasis.hpp"
 #include "sfem/poisson.hpp"
 #include "sfem/spectral.hpp"
@@ -309,6 +310,38 @@ int sfemref_fem_load_sines(int dim, const int* orders, const int* elements, cons
       return v;
     };
     grid_to_dof(fem_load_average(spec), load_dof);
+  });
+}
+
+// FEM load average (poisson.cpp:471-569) of a manufactured case's right-hand
+// side (make_problem, cases.cpp:81-95: -Lap u + shift u, or 1 for constantNd).
+int sfemref_fem_load_case(const char* name, int dim, const int* orders, const int* elements, const double* lengths,
+                          double shift, double* load_dof) {
+  return guarded([&] {
+    const ManufacturedCase& c = manufactured_case(name);
+    require(c.dimension == dim, "fem_load_case: dimension mismatch");
+    ProblemSpec spec = make_problem(c, shift, std::vector<int>(elements, elements + dim),
+                                    std::vector<int>(orders, orders + dim), std::vector<double>(lengths, lengths + dim));
+    grid_to_dof(fem_load_average(spec), load_dof);
+  });
+}
+
+// The reference's end-to-end solve(spec, options) (poisson.cpp:796-808) of a
+// manufactured case with compute_residual: solution (dof layout),
+// residual_rel and error_uniform (NaN when the case has no exact solution).
+int sfemref_solve_case(const char* name, int dim, const int* orders, const int* elements, const double* lengths,
+                       double shift, double* u_dof, double* residual_rel, double* error_uniform) {
+  return guarded([&] {
+    const ManufacturedCase& c = manufactured_case(name);
+    require(c.dimension == dim, "solve_case: dimension mismatch");
+    ProblemSpec spec = make_problem(c, shift, std::vector<int>(elements, elements + dim),
+                                    std::vector<int>(orders, orders + dim), std::vector<double>(lengths, lengths + dim));
+    SolveOptions opt;
+    opt.compute_residual = true;
+    const SolveReport rep = solve(spec, opt);
+    grid_to_dof(rep.solution, u_dof);
+    *residual_rel = rep.residual_rel.value_or(std::nan(""));
+    *error_uniform = rep.error_uniform.value_or(std::nan(""));
   });
 }
 

@@ -38,6 +38,9 @@ def lib():
                                     _dp, _dp, _dp]
         L.sfemref_apply_operator.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, _dp, _dp]
         L.sfemref_fem_load_sines.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, _dp, _dp]
+        L.sfemref_fem_load_case.argtypes = [ctypes.c_char_p, ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, _dp]
+        L.sfemref_solve_case.argtypes = [ctypes.c_char_p, ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, _dp, _dp,
+                                         _dp]
         L.sfemref_uniform.argtypes = [ctypes.c_uint, ctypes.c_longlong, ctypes.c_double, ctypes.c_double, _dp]
         L.sfemref_uniform.restype = None
         _lib = L
@@ -135,3 +138,24 @@ def fem_load_sines(orders, elements, lengths, amp, freq):
                                       _p(np.array(lengths, float)), float(amp), _p(np.array(freq, float)),
                                       _p(out)))
     return out
+
+
+def fem_load_case(name: str, orders, elements, lengths, shift):
+    """fem_load_average of a manufactured case (cases.cpp make_problem)."""
+    N = len(orders)
+    out = np.empty([n * K - 1 for n, K in zip(orders, elements)])
+    _chk(lib().sfemref_fem_load_case(name.encode(), N, (ctypes.c_int * N)(*orders), (ctypes.c_int * N)(*elements),
+                                     _p(np.array(lengths, float)), float(shift), _p(out)))
+    return out
+
+
+def solve_case(name: str, orders, elements, lengths, shift):
+    """The reference's solve(spec, {compute_residual}) of a manufactured case:
+    (u, residual_rel, error_uniform)."""
+    N = len(orders)
+    u = np.empty([n * K - 1 for n, K in zip(orders, elements)])
+    r = np.zeros(1)
+    e = np.zeros(1)
+    _chk(lib().sfemref_solve_case(name.encode(), N, (ctypes.c_int * N)(*orders), (ctypes.c_int * N)(*elements),
+                                  _p(np.array(lengths, float)), float(shift), _p(u), _p(r), _p(e)))
+    return u, float(r[0]), float(e[0])

@@ -861,3 +861,118 @@ def dense_solve(load: np.ndarray, orders, elements, lengths, shift, coefficients
             term = np.kron(term, mats[i][0] if i == t else mats[i][1])
         system = system + (shift if t == N else f[t]) * term
     return np.linalg.solve(system, load.reshape(-1)).reshape(load.shape)
+
+
+# ----------------------------------------------------------------------------
+# The steps either side of the solve: operator application,
+# FEM load averaging, the manufactured cases.  Small sizes only.
+# ----------------------------------------------------------------------------
+
+
+def _along_axis_matmul(mat: np.ndarray, x: np.ndarray, axis: int) -> np.ndarray:
+    return np.moveaxis(np.tensordot(mat, x, axes=([1], [axis])), 0, axis)
+
+
+def apply_operator(v: np.ndarray, orders, elements, lengths, shift, coefficients=None) -> np.ndarray:
+    """A v with A = sum_t f_t (x)_{u!=t} C_u (x) A_t + shift (x)_u C_u (apply_operator,
+    poisson.cpp:749-769; f_t = a_t 4/h_t^2, axis_scale_factors 398-405), using the
+    assembled 1-D matrices of oracle.cpp:13-41 (assemble_global_1d)."""
+    N = v.ndim
+    mats = [assemble_global_1d(orders[i], elements[i]) for i in range(N)]
+    f = axis_scale_factors(lengths, elements)
+    if coefficients is not None:
+        f = [fi * ai for fi, ai in zip(f, coefficients)]
+    out = np.zeros_like(v)
+    for t in range(N + 1):
+        tmp = v
+        for u in range(N):
+            tmp = _along_axis_matmul(mats[u][0] if u == t else mats[u][1], tmp, u)
+        out = out + (shift if t == N else f[t]) * tmp
+    return out
+
+
+def _axis_quad(n: int):
+    """axis_quad (poisson.cpp:481-495): Gauss nodes and w_g * phi_loc(xi_g)."""
+    gn, gw = gauss_legendre(n + 1)
+    nodes = equispaced_nodes(n)
+    wq = np.array([[gw[g] * lagrange_value(nodes, loc, gn[g]) for g in range(n + 1)] for loc in range(n + 1)])
+    return np.array(gn), wq
+
+
+def fem_load_average(orders, elements, lengths, rhs) -> np.ndarray:
+    """fem_load_average (poisson.cpp:499-569) into the dof layout: per element,
+    rhs on the tensor Gauss grid, one weighted-basis contraction per axis, the
+    local load added into the dofs with the boundary contributions dropped.
+    `rhs(x)` takes a list of coordinate arrays (broadcasting)."""
+    N = len(orders)
+    quad = [_axis_quad(n) for n in orders]
+    h = [L / K for L, K in zip(lengths, elements)]
+    ext = [n * K - 1 for n, K in zip(orders, elements)]
+    out = np.zeros(ext)
+    for e in np.ndindex(*elements):
+        grids = np.meshgrid(*[(e[i] + 0.5 * (quad[i][0] + 1.0)) * h[i] for i in range(N)], indexing="ij")
+        vals = rhs(grids)
+        for ax in range(N - 1, -1, -1):
+            vals = _along_axis_matmul(quad[ax][1], vals, ax)
+        # scatter (dof coordinate t = e*n - 1 + loc; boundary dropped)
+        idx = []
+        keep = []
+        for i in range(N):
+            t = e[i] * orders[i] - 1 + np.arange(orders[i] + 1)
+            idx.append(t)
+            keep.append((t >= 0) & (t < ext[i]))
+        sub = vals[np.ix_(*keep)]
+        out[np.ix_(*[t[k] for t, k in zip(idx, keep)])] += sub
+    return out
+
+
+def case_functions(name: str, shift: float):
+    """The reference's manufactured cases (cases.cpp:11-55, make_problem 81-95):
+    (rhs, exact) as functions of a coordinate list; exact None for constantNd."""
+    pi = math.pi
+    if name == "sin1d":
+        def u(x):
+            return np.sin(pi * x[0]) * np.exp(x[0])
+
+        def lap(x):
+            return ((1.0 - pi * pi) * np.sin(pi * x[0]) + 2.0 * pi * np.cos(pi * x[0])) * np.exp(x[0])
+    elif name == "poisson2d":
+        def u(x):
+            return np.sin(2 * pi * x[0]) * np.sin(3 * pi * x[1]) * np.cosh(math.sqrt(2.0) * x[0] - x[1])
+
+        def lap(x):
+            s1, c1 = np.sin(2 * pi * x[0]), np.cos(2 * pi * x[0])
+            s2, c2 = np.sin(3 * pi * x[1]), np.cos(3 * pi * x[1])
+            w = math.sqrt(2.0) * x[0] - x[1]
+            return ((-13.0 * pi * pi + 3.0) * s1 * s2 * np.cosh(w)
+                    + 2.0 * np.sinh(w) * (2.0 * math.sqrt(2.0) * pi * c1 * s2 - 3.0 * pi * s1 * c2))
+    elif name == "poisson3d":
+        def u(x):
+            w = math.sqrt(2.0) * x[0] - x[1] + x[2] / math.sqrt(3.0)
+            return np.sin(2 * pi * x[0]) * np.sin(3 * pi * x[1]) * np.sin(4 * pi * x[2]) * np.cosh(w)
+
+        def lap(x):
+            s1, c1 = np.sin(2 * pi * x[0]), np.cos(2 * pi * x[0])
+            s2, c2 = np.sin(3 * pi * x[1]), np.cos(3 * pi * x[1])
+            s3, c3 = np.sin(4 * pi * x[2]), np.cos(4 * pi * x[2])
+            w = math.sqrt(2.0) * x[0] - x[1] + x[2] / math.sqrt(3.0)
+            return ((-29.0 * pi * pi + 10.0 / 3.0) * s1 * s2 * s3 * np.cosh(w)
+                    + 2.0 * np.sinh(w) * (2.0 * math.sqrt(2.0) * pi * c1 * s2 * s3 - 3.0 * pi * s1 * c2 * s3
+                                          + 4.0 * pi / math.sqrt(3.0) * s1 * s2 * c3))
+    elif name in ("constant1d", "constant2d", "constant3d"):
+        return (lambda x: np.ones_like(x[0])), None
+    else:
+        raise ValueError(f"unknown case '{name}'")
+    return (lambda x: -lap(x) + shift * u(x)), u
+
+
+def dof_coordinates(orders, elements, lengths):
+    """Per-axis coordinate of every dof (axis_coordinate, ndgrid.cpp:71-78)."""
+    out = []
+    for n, K, L in zip(orders, elements, lengths):
+        h = L / K
+        t = np.arange(n * K - 1)
+        node = (t + 1) % n == 0
+        x = np.where(node, h * ((t + 1) // n), h * (t // n + (t % n + 1) / n))
+        out.append(x)
+    return out

@@ -27,7 +27,8 @@ __all__ = [
     "Error", "lib", "lib_path", "Context", "SpectralTable", "TableSet", "ProblemSpec", "SolveOptions",
     "SolveReport", "Plan", "GridFunction1D", "CoefficientArray1D", "GridFunctionND", "solve_with_load",
     "solve_dof", "synthesize", "decompose", "decompose_weighted", "lines", "lines_device", "DECOMPOSE_WEIGHTED",
-    "DECOMPOSE", "SYNTHESIZE", "default_context", "HEADER_SYMBOLS",
+    "DECOMPOSE", "SYNTHESIZE", "default_context", "HEADER_SYMBOLS", "Field", "solve", "FIELD_CONSTANT",
+    "FIELD_SINES", "FIELD_SIN1D", "FIELD_POISSON2D", "FIELD_POISSON3D", "CASE_FIELDS",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -36,6 +37,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.environ.get("SFEM_LIB") or os.path.join(_HERE, "libsfem_b200.so")
 
 DECOMPOSE_WEIGHTED, DECOMPOSE, SYNTHESIZE = 0, 1, 2
+# built-in right-hand sides of sfem_cuda_fem_load (include/sfem_cuda.h)
+FIELD_CONSTANT, FIELD_SINES, FIELD_SIN1D, FIELD_POISSON2D, FIELD_POISSON3D = 0, 1, 2, 3, 4
+# the reference's manufactured case names (cases.hpp:20) -> field
+CASE_FIELDS = {"sin1d": FIELD_SIN1D, "poisson2d": FIELD_POISSON2D, "poisson3d": FIELD_POISSON3D,
+               "constant1d": FIELD_CONSTANT, "constant2d": FIELD_CONSTANT, "constant3d": FIELD_CONSTANT}
 
 
 class Error(RuntimeError):
@@ -81,6 +87,10 @@ _SIGS = [
     ("sfem_cuda_solve_host_batch", ctypes.c_int, [_vp, ctypes.c_longlong, ctypes.POINTER(_dp), ctypes.POINTER(_dp)]),
     ("sfem_cuda_solve_device_timed", ctypes.c_int,
      [_vp, _vp, ctypes.c_longlong, ctypes.c_int, _dp, _dp]),
+    ("sfem_cuda_fem_load", ctypes.c_int, [_vp, ctypes.c_int, _dp, ctypes.c_int, _vp, ctypes.c_longlong, _vp]),
+    ("sfem_cuda_apply_operator", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _vp]),
+    ("sfem_cuda_residual", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _dp]),
+    ("sfem_cuda_max_error", ctypes.c_int, [_vp, ctypes.c_int, _dp, ctypes.c_int, _vp, ctypes.c_longlong, _dp]),
     ("sfem_cuda_dist_create", ctypes.c_int,
      [_vp, ctypes.c_int, _ip, _ip, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
     ("sfem_cuda_dist_destroy", ctypes.c_int, [_vp]),
@@ -430,6 +440,33 @@ class Plan:
                                                 ctypes.byref(total), per))
         return total.value, list(per)
 
+    # ---- the steps either side of the solve, device pointers ----
+    def fem_load_device(self, field: "Field", d_load: int, pitch: Optional[int] = None, stream: int = 0):
+        """sfem_cuda_fem_load: FEM load of `field` into a padded device tensor."""
+        prm = _f64(field.params if len(field.params) else [0.0])
+        _check(lib.sfem_cuda_fem_load(self.handle, field.kind, _dptr(prm), len(field.params), ctypes.c_void_p(d_load),
+                                      self.pitch if pitch is None else pitch, ctypes.c_void_p(stream or None)))
+
+    def apply_operator_device(self, d_v: int, d_y: int, pitch: Optional[int] = None, stream: int = 0):
+        """sfem_cuda_apply_operator: y = A v."""
+        _check(lib.sfem_cuda_apply_operator(self.handle, ctypes.c_void_p(d_v), ctypes.c_void_p(d_y),
+                                            self.pitch if pitch is None else pitch, ctypes.c_void_p(stream or None)))
+
+    def residual_device(self, d_u: int, d_f: int, pitch: Optional[int] = None) -> float:
+        """sfem_cuda_residual: max|A u - f| / max|f|."""
+        r = ctypes.c_double()
+        _check(lib.sfem_cuda_residual(self.handle, ctypes.c_void_p(d_u), ctypes.c_void_p(d_f),
+                                      self.pitch if pitch is None else pitch, ctypes.byref(r)))
+        return r.value
+
+    def max_error_device(self, field: "Field", d_u: int, pitch: Optional[int] = None) -> float:
+        """sfem_cuda_max_error: max |u - u_exact| over the dofs."""
+        prm = _f64(field.params if len(field.params) else [0.0])
+        e = ctypes.c_double()
+        _check(lib.sfem_cuda_max_error(self.handle, field.kind, _dptr(prm), len(field.params), ctypes.c_void_p(d_u),
+                                       self.pitch if pitch is None else pitch, ctypes.byref(e)))
+        return e.value
+
     def solve_classes(self, load: GridFunctionND) -> GridFunctionND:
         N = self.spec.dimension
         ins = [_f64(c) for c in load.classes]
@@ -471,3 +508,74 @@ def solve_with_load(spec: ProblemSpec, load, tables: Optional[TableSet] = None,
     else:
         sol, sec = plan.solve_host(load)
     return SolveReport(solution=sol, seconds_solve=sec)
+
+
+@dataclass
+class Field:
+    """A built-in right-hand side (the device stand-in for ProblemSpec::rhs /
+    exact, poisson.hpp:39-40).  kind: FIELD_*; params as sfem_cuda_fem_load."""
+    kind: int
+    params: Sequence[float] = ()
+
+    @staticmethod
+    def constant(value: float = 1.0) -> "Field":
+        return Field(FIELD_CONSTANT, [float(value)])
+
+    @staticmethod
+    def sines(amp: float, wave_numbers: Sequence[float]) -> "Field":
+        return Field(FIELD_SINES, [float(amp)] + [float(k) for k in wave_numbers])
+
+    @staticmethod
+    def case(name: str) -> "Field":
+        """The reference's manufactured case by name (cases.cpp:61-78)."""
+        if name not in CASE_FIELDS:
+            raise Error(f"unknown case '{name}' (known: {', '.join(CASE_FIELDS)})")
+        kind = CASE_FIELDS[name]
+        return Field.constant(1.0) if kind == FIELD_CONSTANT else Field(kind, [])
+
+    @property
+    def has_exact(self) -> bool:
+        return self.kind != FIELD_CONSTANT
+
+
+def _torch():
+    import torch  # device memory / events only (plumbing)
+    if not torch.cuda.is_available():
+        raise Error("solve: no CUDA device")
+    return torch
+
+
+def solve(spec: ProblemSpec, rhs: Field, options: Optional[SolveOptions] = None,
+          ctx: Optional[Context] = None) -> SolveReport:
+    """solve (poisson.hpp:86; poisson.cpp:796-808) with every step on the device:
+    FEM load (seconds_load), the fused solve (seconds_solve), and on request
+    the residual check and, for fields with a known solution, error_uniform.
+    The solution comes back as a dense dof tensor."""
+    options = options or SolveOptions()
+    if options.algorithm != "full":
+        raise Error("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path")
+    torch = _torch()
+    plan = Plan(spec, ctx)
+    dev = torch.device("cuda", plan.ctx.device)
+    f = torch.empty(plan.padded_shape, dtype=torch.float64, device=dev)
+    u = torch.empty_like(f)
+    s = torch.cuda.ExternalStream(plan.ctx.stream, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(s):
+        ev[0].record(s)
+        plan.fem_load_device(rhs, f.data_ptr())
+        ev[1].record(s)
+        u.copy_(f)
+        ev[2].record(s)
+        plan.solve_device(u.data_ptr())
+        ev[3].record(s)
+    s.synchronize()
+    rep = SolveReport(solution=u[..., :plan.extents[-1]].cpu().numpy().copy(),
+                      seconds_load=ev[0].elapsed_time(ev[1]) / 1e3,
+                      seconds_solve=ev[2].elapsed_time(ev[3]) / 1e3)
+    if options.compute_residual:
+        rep.residual_rel = plan.residual_device(u.data_ptr(), f.data_ptr())
+    if rhs.has_exact:
+        rep.error_uniform = plan.max_error_device(rhs, u.data_ptr())
+    return rep

@@ -28,6 +28,7 @@
 
 #include "../../include/sfem_cuda.h"
 #include "dist.cuh"
+#include "fem_ops.cuh"
 #include "sweep.cuh"
 #include "table.hpp"
 
@@ -416,6 +417,9 @@ struct sfem_plan_s {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> kev;
   bool use_fast = true;
+  // operator / residual scratch (P and Q tensors, padded) and reduction slots
+  double* opwork[2] = {nullptr, nullptr};
+  unsigned long long* dred = nullptr;
 };
 
 namespace {
@@ -648,6 +652,116 @@ std::vector<long long> balanced(long long n, int parts, std::vector<long long>& 
 
 }  // namespace
 
+namespace {
+
+int device_sms(int device) {
+  int n = 0;
+  ck(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
+  return n;
+}
+
+// Field description for the load / error kernels, validated against the plan.
+FieldArgs make_field(const sfem_plan_s* p, int field, const double* params, int nparams) {
+  FieldArgs fa{};
+  fa.kind = field;
+  fa.dim = p->dim;
+  fa.shift = p->shift;
+  auto unit_coeffs = [&] {
+    for (double c : p->coeffs)
+      require(c == 1.0, "fem_load: the manufactured cases are defined for unit coefficients (cases.cpp:81-95)");
+  };
+  switch (field) {
+    case SFEM_FIELD_CONSTANT:
+      require(params && nparams >= 1, "fem_load: CONSTANT needs params[0]");
+      fa.p[0] = params[0];
+      break;
+    case SFEM_FIELD_SINES: {
+      require(params && nparams >= 1 + p->dim, "fem_load: SINES needs amp and one wave number per axis");
+      fa.p[0] = params[0];
+      double denom = p->shift;
+      for (int i = 0; i < p->dim; ++i) {
+        fa.p[1 + i] = params[1 + i];
+        const double k = params[1 + i] * M_PI;
+        denom += p->coeffs[i] * k * k;
+      }
+      fa.p[1 + kMaxDim] = denom != 0.0 ? params[0] / denom : 0.0;
+      break;
+    }
+    case SFEM_FIELD_SIN1D:
+      require(p->dim == 1, "fem_load: case sin1d is 1-D");
+      unit_coeffs();
+      break;
+    case SFEM_FIELD_POISSON2D:
+      require(p->dim == 2, "fem_load: case poisson2d is 2-D");
+      unit_coeffs();
+      break;
+    case SFEM_FIELD_POISSON3D:
+      require(p->dim == 3, "fem_load: case poisson3d is 3-D");
+      unit_coeffs();
+      break;
+    default:
+      fail("fem_load: unknown field " + std::to_string(field));
+  }
+  return fa;
+}
+
+// dof-tensor strides (last axis padded to pitch)
+std::vector<long long> dof_strides(const sfem_plan_s* p, long long pitch) {
+  std::vector<long long> st(p->dim);
+  st[p->dim - 1] = 1;
+  if (p->dim >= 2) st[p->dim - 2] = pitch;
+  for (int i = p->dim - 3; i >= 0; --i) st[i] = st[i + 1] * p->ext[i + 1];
+  return st;
+}
+
+size_t padded_elems(const sfem_plan_s* p, long long pitch) { return static_cast<size_t>(p->rows) * pitch; }
+
+// A v into q_out (or, with f, max|A v - f| and max|f| into p->dred): one sweep
+// per axis 0..N-1 carrying P (scratch) and Q (q_out or scratch), fem_ops.cu.
+void apply_sweeps(sfem_plan_s* p, const double* v, double* q_out, const double* f, long long pitch,
+                  cudaStream_t s) {
+  const size_t elems = padded_elems(p, pitch);
+  const int nbuf = f ? 2 : 1;
+  for (int b = 0; b < nbuf; ++b)
+    if (!p->opwork[b]) ck(cudaMalloc(&p->opwork[b], elems * sizeof(double)), "cudaMalloc(operator scratch)");
+  double* P = p->opwork[0];
+  double* Q = f ? p->opwork[1] : q_out;
+  const std::vector<long long> st = dof_strides(p, pitch);
+  const int N = p->dim;
+  for (int a = 0; a < N; ++a) {
+    OpAxisArgs A{};
+    const HostTable& h = p->tables[a]->host;
+    A.n = p->orders[a];
+    A.K = p->elements[a];
+    A.L = p->ext[a];
+    A.pitch = pitch;
+    A.last = p->ext[N - 1];
+    A.fac = p->factors[a];
+    A.shift = p->shift;
+    const int np = A.n + 1;
+    for (int r = 0; r < np; ++r)
+      for (int c = 0; c < np; ++c) {
+        A.M[r][c] = h.mass[static_cast<size_t>(r) * np + c];
+        A.S[r][c] = h.stiffness[static_cast<size_t>(r) * np + c];
+      }
+    const bool rows = a == N - 1;
+    A.outer = 1;
+    for (int i = 0; i < (rows ? N - 1 : a); ++i) A.outer *= p->ext[i];
+    A.inner = rows ? 1 : st[a];
+    const bool first = a == 0, last = a == N - 1;
+    ck(launch_op_axis(first ? v : P, P, Q, f, A, rows, first, last, f != nullptr && last, p->dred, s),
+       "operator sweep");
+  }
+}
+
+double red_to_double(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof d);
+  return d;
+}
+
+}  // namespace
+
 extern "C" {
 
 int sfem_cuda_version(void) { return 100; }
@@ -847,6 +961,9 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
       if (p->e_comp[b]) cudaEventDestroy(p->e_comp[b]);
       if (p->e_out[b]) cudaEventDestroy(p->e_out[b]);
     }
+    for (auto* w : p->opwork)
+      if (w) cudaFree(w);
+    if (p->dred) cudaFree(p->dred);
     if (p->pin) cudaStreamDestroy(p->pin);
     if (p->pout) cudaStreamDestroy(p->pout);
     for (auto& t : p->owned)
@@ -1212,6 +1329,92 @@ int sfem_cuda_dist_phase(sfem_dist d, int phase, double* x, double* y, double* b
       default:
         fail("dist_phase: unknown phase");
     }
+  });
+}
+
+
+int sfem_cuda_fem_load(sfem_plan p, int field, const double* params, int nparams, double* d_load, long long pitch,
+                       void* stream) {
+  return guarded([&] {
+    require(p && d_load, "fem_load: null argument");
+    require(pitch >= p->ext[p->dim - 1], "fem_load: pitch smaller than the last extent");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->ctx->stream;
+    const FieldArgs fa = make_field(p, field, params, nparams);
+    LoadArgs a{};
+    a.dim = p->dim;
+    const std::vector<long long> st = dof_strides(p, pitch);
+    for (int i = 0; i < p->dim; ++i) {
+      a.n[i] = p->orders[i];
+      a.np[i] = p->orders[i] + 1;
+      a.K[i] = p->elements[i];
+      a.h[i] = p->lengths[i] / p->elements[i];
+      a.ext[i] = p->ext[i];
+      a.st[i] = st[i];
+      std::vector<double> nodes, wq;
+      load_quadrature(p->orders[i], nodes, wq);
+      for (int g = 0; g <= p->orders[i]; ++g) a.gnode[i][g] = nodes[g];
+      std::copy(wq.begin(), wq.end(), a.wq[i]);
+    }
+    ck(cudaMemsetAsync(d_load, 0, padded_elems(p, pitch) * sizeof(double), s), "memset(load)");
+    ck(launch_fem_load(d_load, a, fa, device_sms(p->ctx->device), s), "fem_load kernel");
+  });
+}
+
+int sfem_cuda_apply_operator(sfem_plan p, const double* d_v, double* d_y, long long pitch, void* stream) {
+  return guarded([&] {
+    require(p && d_v && d_y, "apply_operator: null argument");
+    require(d_v != d_y, "apply_operator: v and y must be distinct");
+    require(pitch >= p->ext[p->dim - 1], "apply_operator: pitch smaller than the last extent");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->ctx->stream;
+    apply_sweeps(p, d_v, d_y, nullptr, pitch, s);
+  });
+}
+
+int sfem_cuda_residual(sfem_plan p, const double* d_u, const double* d_f, long long pitch, double* residual_rel) {
+  return guarded([&] {
+    require(p && d_u && d_f && residual_rel, "residual: null argument");
+    require(pitch >= p->ext[p->dim - 1], "residual: pitch smaller than the last extent");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = p->ctx->stream;
+    if (!p->dred) ck(cudaMalloc(&p->dred, 2 * sizeof(unsigned long long)), "cudaMalloc(reduction)");
+    ck(cudaMemsetAsync(p->dred, 0, 2 * sizeof(unsigned long long), s), "memset");
+    apply_sweeps(p, d_u, nullptr, d_f, pitch, s);
+    unsigned long long h[2];
+    ck(cudaMemcpyAsync(h, p->dred, sizeof h, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    const double num = red_to_double(h[0]), den = red_to_double(h[1]);
+    *residual_rel = num / (den > 0 ? den : 1.0);  // poisson.cpp:786-788
+  });
+}
+
+int sfem_cuda_max_error(sfem_plan p, int field, const double* params, int nparams, const double* d_u, long long pitch,
+                        double* error) {
+  return guarded([&] {
+    require(p && d_u && error, "max_error: null argument");
+    require(field != SFEM_FIELD_CONSTANT, "max_error: the CONSTANT field has no closed-form solution");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = p->ctx->stream;
+    const FieldArgs fa = make_field(p, field, params, nparams);
+    ErrArgs a{};
+    a.dim = p->dim;
+    a.total = 1;
+    const std::vector<long long> st = dof_strides(p, pitch);
+    for (int i = 0; i < p->dim; ++i) {
+      a.n[i] = p->orders[i];
+      a.ext[i] = p->ext[i];
+      a.st[i] = st[i];
+      a.h[i] = p->lengths[i] / p->elements[i];
+      a.total *= p->ext[i];
+    }
+    if (!p->dred) ck(cudaMalloc(&p->dred, 2 * sizeof(unsigned long long)), "cudaMalloc(reduction)");
+    ck(cudaMemsetAsync(p->dred, 0, 2 * sizeof(unsigned long long), s), "memset");
+    ck(launch_max_error(d_u, a, fa, p->dred, device_sms(p->ctx->device), s), "max_error kernel");
+    unsigned long long h[2];
+    ck(cudaMemcpyAsync(h, p->dred, sizeof h, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    *error = red_to_double(h[0]);
   });
 }
 

@@ -538,6 +538,19 @@ std::vector<double> interior_solution(const Interior& es, int order, double lamb
 
 }  // namespace
 
+void load_quadrature(int n, std::vector<double>& nodes, std::vector<double>& weighted) {
+  // axis_quad (reference poisson.cpp:481-495): (n+1)-point Gauss rule and
+  // weighted[loc * (n+1) + g] = w_g * phi_loc(xi_g) on the equispaced nodes
+  if (n < 1 || n > 9) fail("fem_load: order " + std::to_string(n) + " outside [1, 9]");
+  std::vector<double> w;
+  gauss_legendre(n + 1, nodes, w);
+  std::vector<double> eq(n + 1);
+  for (int k = 0; k <= n; ++k) eq[k] = static_cast<double>(2 * k - n) / static_cast<double>(n);
+  weighted.assign(static_cast<size_t>(n + 1) * (n + 1), 0.0);
+  for (int loc = 0; loc <= n; ++loc)
+    for (int g = 0; g <= n; ++g) weighted[static_cast<size_t>(loc) * (n + 1) + g] = w[g] * lagrange_value(eq, loc, nodes[g]);
+}
+
 HostTable build_host_table(int n, int K) {
   if (K < 2) fail("spectral table: need at least two elements");
   const Element em = build_element(n);

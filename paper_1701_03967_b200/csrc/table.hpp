@@ -58,4 +58,8 @@ struct DeviceTableData {
 
 DeviceTableData derive_device_data(const HostTable& t);
 
+// Gauss nodes (n+1 points) and weighted[loc*(n+1)+g] = w_g phi_loc(xi_g) of the
+// load averaging (reference axis_quad, poisson.cpp:481-495).
+void load_quadrature(int n, std::vector<double>& nodes, std::vector<double>& weighted);
+
 }  // namespace sfem_b200

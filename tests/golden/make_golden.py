@@ -33,6 +33,26 @@ SOLVES = {
     "2d_n4_K7": ([4, 4], [7, 7], [1.0, 1.0], 0.5, 17),
 }
 
+# (name, case, orders, elements, lengths, shift)
+FEM_LOADS = [
+    ("sin1d_n4_K6", "sin1d", [4], [6], [1.0], 1.0),
+    ("poisson2d_n3n2", "poisson2d", [3, 2], [5, 4], [1.0, 1.3], 0.5),
+    ("poisson3d_n2n3n2", "poisson3d", [2, 3, 2], [3, 2, 4], [1.0, 1.0, 1.0], 0.25),
+    ("constant2d_n9", "constant2d", [9, 9], [3, 2], [1.0, 1.0], 0.0),
+    ("sines_c3_small", "sines", [9, 9], [8, 8], [1.0, 1.0], 0.0),
+]
+OPERATORS = {
+    "1d_n5_K7": ([5], [7], [1.0], 0.75, 21),
+    "2d_mixed": ([3, 2], [5, 4], [1.0, 1.3], 0.5, 22),
+    "3d_mixed": ([2, 9, 1], [3, 2, 4], [1.0, 0.5, 2.0], 0.0, 23),
+    "2d_n9_K8": ([9, 9], [8, 8], [1.0, 1.0], 1.0, 24),
+}
+CASE_SOLVES = [
+    ("sin1d_n4_K6", "sin1d", [4], [6], [1.0], 1.0),
+    ("poisson2d_n9_K8", "poisson2d", [9, 9], [8, 8], [1.0, 1.0], 0.0),
+    ("poisson3d_n3_K4", "poisson3d", [3, 3, 3], [4, 4, 4], [1.0, 1.0, 1.0], 0.5),
+]
+
 
 def main():
     out = {}
@@ -87,7 +107,30 @@ def main():
     out["c3_small/load"] = load
     out["c3_small/u"] = u
     np.savez_compressed(os.path.join(HERE, "solves.npz"), **out)
-    for f in ("trig", "tables", "lines", "solves"):
+    # the steps either side of the solve: FEM loads of the
+    # manufactured cases / the config-3 sines, operator applications, and the
+    # reference's end-to-end solve() of the cases (residual, uniform error)
+    out = {}
+    for name, case, orders, elements, lengths, shift in FEM_LOADS:
+        if case == "sines":
+            load = R.fem_load_sines(orders, elements, lengths, 9 * np.pi ** 2 + 1, [1.0, 2.0])
+        else:
+            load = R.fem_load_case(case, orders, elements, lengths, shift)
+        out[f"load/{name}"] = load
+        out[f"load/{name}/meta"] = np.array(orders + elements + lengths + [shift], float)
+    for name, (orders, elements, lengths, shift, seed) in OPERATORS.items():
+        ext = [n * K - 1 for n, K in zip(orders, elements)]
+        v = R.uniform(seed, int(np.prod(ext))).reshape(ext)
+        out[f"op/{name}/v"] = v
+        out[f"op/{name}/Av"] = R.apply_operator(v, orders, elements, lengths, shift)
+        out[f"op/{name}/meta"] = np.array(orders + elements + lengths + [shift], float)
+    for name, case, orders, elements, lengths, shift in CASE_SOLVES:
+        u, res, err = R.solve_case(case, orders, elements, lengths, shift)
+        out[f"case/{name}/u"] = u
+        out[f"case/{name}/residual_error"] = np.array([res, err])
+        out[f"case/{name}/meta"] = np.array(orders + elements + lengths + [shift], float)
+    np.savez_compressed(os.path.join(HERE, "fem.npz"), **out)
+    for f in ("trig", "tables", "lines", "solves", "fem"):
         print(f, os.path.getsize(os.path.join(HERE, f + ".npz")))
 
 

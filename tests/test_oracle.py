@@ -178,6 +178,56 @@ def test_oracle_solves_match_reference_golden():
     assert rel_l2(u, g["c3_small/u"]) <= 1e-12
 
 
+def _meta(meta):
+    N = (len(meta) - 1) // 3
+    return ([int(v) for v in meta[:N]], [int(v) for v in meta[N:2 * N]], list(meta[2 * N:3 * N]), float(meta[-1]))
+
+
+def test_oracle_fem_loads_match_reference_golden():
+    # fem_load_average (poisson.cpp:499-569) of the manufactured cases and the config-3 sines
+    g = load_golden("fem")
+    names = [k[5:-5] for k in g.files if k.startswith("load/") and k.endswith("/meta")]
+    assert len(names) == 5
+    for name in names:
+        orders, elements, lengths, shift = _meta(g[f"load/{name}/meta"])
+        if name.startswith("sines"):
+            def rhs(x):
+                return (9 * np.pi ** 2 + 1) * np.sin(np.pi * x[0]) * np.sin(2 * np.pi * x[1])
+        else:
+            rhs, _ = O.case_functions(name.split("_")[0], shift)
+        assert rel_l2(O.fem_load_average(orders, elements, lengths, rhs), g[f"load/{name}"]) <= 1e-13, name
+
+
+def test_oracle_operator_matches_reference_golden():
+    # apply_operator (poisson.cpp:749-769) on seeded vectors
+    g = load_golden("fem")
+    names = [k[3:-5] for k in g.files if k.startswith("op/") and k.endswith("/meta")]
+    assert len(names) == 4
+    for name in names:
+        orders, elements, lengths, shift = _meta(g[f"op/{name}/meta"])
+        got = O.apply_operator(g[f"op/{name}/v"], orders, elements, lengths, shift)
+        assert rel_l2(got, g[f"op/{name}/Av"]) <= 1e-13, name
+
+
+def test_oracle_case_solves_match_reference_golden():
+    # the reference's solve() of its manufactured cases: u, residual_rel and
+    # error_uniform (max_error_vs, ndgrid.cpp:80-101) restated
+    g = load_golden("fem")
+    names = [k[5:-5] for k in g.files if k.startswith("case/") and k.endswith("/meta")]
+    assert len(names) == 3
+    for name in names:
+        orders, elements, lengths, shift = _meta(g[f"case/{name}/meta"])
+        rhs, exact = O.case_functions(name.split("_")[0], shift)
+        load = O.fem_load_average(orders, elements, lengths, rhs)
+        u = O.solve_full_diagonalization(load, orders, elements, lengths, shift)
+        assert rel_l2(u, g[f"case/{name}/u"]) <= 1e-12, name
+        res, err = g[f"case/{name}/residual_error"]
+        Au = O.apply_operator(u, orders, elements, lengths, shift)
+        assert np.abs(Au - load).max() / np.abs(load).max() <= 1e-10 and res <= 1e-10, name
+        X = np.meshgrid(*O.dof_coordinates(orders, elements, lengths), indexing="ij")
+        assert abs(np.abs(u - exact(X)).max() - err) <= 1e-12 * max(1.0, err), name
+
+
 # ---- the compiled reference (oracle/_ref), when built here ----------------
 
 needs_ref = pytest.mark.skipif(not reflib.available(), reason="oracle/_ref not built")
