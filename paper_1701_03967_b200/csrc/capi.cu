@@ -420,6 +420,8 @@ struct sfem_plan_s {
   // operator / residual scratch (P and Q tensors, padded) and reduction slots
   double* opwork[2] = {nullptr, nullptr};
   unsigned long long* dred = nullptr;
+  double* load_vec = nullptr;  // per-axis 1-D loads of separable fields
+  size_t load_vec_cap = 0;
 };
 
 namespace {
@@ -964,6 +966,7 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
     for (auto* w : p->opwork)
       if (w) cudaFree(w);
     if (p->dred) cudaFree(p->dred);
+    if (p->load_vec) cudaFree(p->load_vec);
     if (p->pin) cudaStreamDestroy(p->pin);
     if (p->pout) cudaStreamDestroy(p->pout);
     for (auto& t : p->owned)
@@ -1355,6 +1358,46 @@ int sfem_cuda_fem_load(sfem_plan p, int field, const double* params, int nparams
       load_quadrature(p->orders[i], nodes, wq);
       for (int g = 0; g <= p->orders[i]; ++g) a.gnode[i][g] = nodes[g];
       std::copy(wq.begin(), wq.end(), a.wq[i]);
+    }
+    if (field == SFEM_FIELD_CONSTANT || field == SFEM_FIELD_SINES) {
+      // separable: per-axis assembled 1-D loads of g_i (1, or sin(k_i pi x)),
+      // following the element loop of poisson.cpp:499-569 per axis
+      SepArgs sa{};
+      sa.dim = p->dim;
+      sa.total = static_cast<long long>(padded_elems(p, pitch));
+      sa.amp = fa.p[0];
+      sa.pitch = pitch;
+      std::vector<double> B;
+      for (int i = 0; i < p->dim; ++i) {
+        const int n = a.n[i], np = n + 1, K = a.K[i];
+        sa.ext[i] = a.ext[i];
+        sa.st[i] = a.st[i];
+        sa.boff[i] = static_cast<long long>(B.size());
+        B.resize(B.size() + a.ext[i], 0.0);
+        double* Bi = B.data() + sa.boff[i];
+        for (int e = 0; e < K; ++e)
+          for (int loc = 0; loc <= n; ++loc) {
+            const long long t = static_cast<long long>(e) * n - 1 + loc;
+            if (t < 0 || t >= a.ext[i]) continue;
+            double acc = 0;
+            for (int g = 0; g < np; ++g) {
+              const double x = (e + 0.5 * (a.gnode[i][g] + 1.0)) * a.h[i];
+              const double gv = field == SFEM_FIELD_SINES ? std::sin(fa.p[1 + i] * M_PI * x) : 1.0;
+              acc += a.wq[i][loc * np + g] * gv;
+            }
+            Bi[t] += acc;
+          }
+      }
+      if (B.size() > p->load_vec_cap) {
+        if (p->load_vec) ck(cudaFree(p->load_vec), "cudaFree");
+        p->load_vec = nullptr;
+        ck(cudaMalloc(&p->load_vec, B.size() * sizeof(double)), "cudaMalloc(load vectors)");
+        p->load_vec_cap = B.size();
+      }
+      ck(cudaMemcpyAsync(p->load_vec, B.data(), B.size() * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+      ck(launch_fem_load_separable(d_load, p->load_vec, sa, device_sms(p->ctx->device), s), "fem_load kernel");
+      ck(cudaStreamSynchronize(s), "sync");  // B (host) is released on return
+      return;
     }
     ck(cudaMemsetAsync(d_load, 0, padded_elems(p, pitch) * sizeof(double), s), "memset(load)");
     ck(launch_fem_load(d_load, a, fa, device_sms(p->ctx->device), s), "fem_load kernel");

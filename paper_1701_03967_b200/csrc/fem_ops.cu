@@ -160,6 +160,30 @@ __global__ void fem_load_color(double* __restrict__ out, const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------
+// Separable fields (constant, product of sines): the element loads are rank
+// one, so the assembled load is amp * outer product of the assembled 1-D
+// loads B_i (sum over the elements containing dof t_i of b_i[e][loc]); one
+// write per dof.  B = concatenated per-axis vectors, boff[i] their offsets.
+// ---------------------------------------------------------------------------
+__global__ void fem_load_separable(double* __restrict__ out, const double* __restrict__ Bv, SepArgs a) {
+  for (long long l = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; l < a.total;
+       l += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long rem = l, off = 0;
+    double v = a.amp;
+    bool pad = false;
+    for (int i = a.dim - 1; i >= 0; --i) {
+      const long long ext = i == a.dim - 1 ? a.pitch : a.ext[i];
+      const long long t = rem % ext;
+      rem /= ext;
+      off += t * a.st[i];
+      if (t >= a.ext[i]) pad = true;
+      else v *= __ldg(Bv + a.boff[i] + t);
+    }
+    out[off] = pad ? 0.0 : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Operator sweeps.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
@@ -414,6 +438,13 @@ cudaError_t launch_fem_load(double* out, const LoadArgs& a, const FieldArgs& fa,
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_fem_load_separable(double* out, const double* Bv, const SepArgs& a, int num_sms, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>(
+      std::max<long long>(1, std::min<long long>((a.total + 255) / 256, 32LL * num_sms)));
+  femops::fem_load_separable<<<grid, 256, 0, s>>>(out, Bv, a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_max_error(const double* u, const ErrArgs& a, const FieldArgs& fa, unsigned long long* red,

@@ -45,6 +45,16 @@ struct OpAxisArgs {
   double M[kMaxNP][kMaxNP], S[kMaxNP][kMaxNP];
 };
 
+// Separable load: out[t] = amp * prod_i B_i[t_i] over the padded tensor
+// (total = rows * pitch elements; padding written as zero).
+struct SepArgs {
+  int dim;
+  long long total;
+  double amp;
+  long long ext[kMaxDim], st[kMaxDim], boff[kMaxDim];
+  long long pitch;
+};
+
 struct ErrArgs {
   int dim;
   long long total;
@@ -56,6 +66,7 @@ struct ErrArgs {
 cudaError_t launch_op_axis(const double* pin, double* pout, double* q, const double* f, const OpAxisArgs& a,
                            bool rows, bool first, bool last, bool resid, unsigned long long* red, cudaStream_t s);
 cudaError_t launch_fem_load(double* out, const LoadArgs& a, const FieldArgs& fa, int num_sms, cudaStream_t s);
+cudaError_t launch_fem_load_separable(double* out, const double* Bv, const SepArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_max_error(const double* u, const ErrArgs& a, const FieldArgs& fa, unsigned long long* red,
                              int num_sms, cudaStream_t s);
 

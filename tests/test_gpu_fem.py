@@ -71,10 +71,10 @@ def test_fem_load_matches_reference_golden(sfem):
 
 def test_fem_load_is_deterministic(sfem):
     plan = _plan(sfem, [9, 9], [32, 16], [1.0, 1.0], 0.0)
-    f = sfem.Field.sines(3.0, [1.0, 2.0])
-    a = _to_host(plan, _device_load(sfem, plan, f))
-    b = _to_host(plan, _device_load(sfem, plan, f))
-    assert np.array_equal(a, b)
+    for f in (sfem.Field.sines(3.0, [1.0, 2.0]), sfem.Field.case("poisson2d")):  # separable / general path
+        a = _to_host(plan, _device_load(sfem, plan, f))
+        b = _to_host(plan, _device_load(sfem, plan, f))
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("orders,elements,lengths,shift", [
@@ -199,3 +199,24 @@ def test_operator_matches_reference_cpu_at_size(sfem):
     y = torch.zeros_like(d)
     plan.apply_operator_device(d.data_ptr(), y.data_ptr())
     assert rel_l2(_to_host(plan, y), reflib.apply_operator(v, orders, elements, lengths, shift)) <= 1e-12
+
+
+@needs_ref
+def test_residual_of_our_solve_tracks_the_reference(sfem):
+    # the residual check is dominated by rounding times cond(A) (it grows like
+    # K^2..K^3); ours must stay within a small factor of the reference's own
+    # solve() on the same problem, and the device operator must reproduce the
+    # reference's residual of the reference's solution.
+    for case, orders, K in (("poisson3d", [9, 9, 9], 24), ("poisson2d", [9, 9], 256)):
+        N = len(orders)
+        els, L = [K] * N, [1.0] * N
+        plan = _plan(sfem, orders, els, L, 0.0)
+        load = reflib.fem_load_case(case, orders, els, L, 0.0)
+        u_ref, r_ref, _ = reflib.solve_case(case, orders, els, L, 0.0)
+        df = _to_dev(plan, load)
+        du = df.clone()
+        plan.solve_device(du.data_ptr())
+        r_ours = plan.residual_device(du.data_ptr(), df.data_ptr())
+        r_dev_of_ref = plan.residual_device(_to_dev(plan, u_ref).data_ptr(), df.data_ptr())
+        assert r_ours <= 3.0 * r_ref, (case, r_ours, r_ref)
+        assert r_dev_of_ref == pytest.approx(r_ref, rel=0.5), (case, r_dev_of_ref, r_ref)
