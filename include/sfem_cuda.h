@@ -168,6 +168,35 @@ int sfem_cuda_dist_destroy(sfem_dist dist);
 int sfem_cuda_dist_shape(sfem_dist dist, long long* info, long long* send_counts, long long* recv_counts);
 int sfem_cuda_dist_phase(sfem_dist dist, int phase, double* d_x, double* d_y, double* d_buf, void* stream);
 
+/* ---- Multi-GPU with the exchanges fused into the sweeps over NVLink ----
+ * 3-D problems whose axes 0 and 1 have K = 64 tables (config 4), 1..8 ranks,
+ * one process per GPU.  No NCCL on the data path: the axis-1 forward sweep
+ * TMA-stores each finished tile straight into the owning rank's y-slab (peer
+ * memory), and the fused axis-0 sweep (forward + divide + inverse) stores its
+ * tiles straight back into the source ranks' x-slabs.  Rank r's buffers are
+ * plan-owned: x-slab [L1][lx][pitch] (axis-0 rows x0.., laid out y, x, z) and
+ * y-slab [ly][L0][pitch] (axis-1 rows y0..).  One solve:
+ *   PEER_FORWARD, PEER_BARRIER, PEER_AXIS0, PEER_BARRIER, PEER_INVERSE.
+ * Replaces run_full_diagonalization (poisson.cpp:637-669), sharded. */
+typedef struct sfem_peer_s* sfem_peer;
+enum { SFEM_PEER_FORWARD = 0, SFEM_PEER_AXIS0 = 1, SFEM_PEER_INVERSE = 2, SFEM_PEER_BARRIER = 3 };
+int sfem_cuda_peer_create(sfem_ctx ctx, int dim, const int* orders, const int* elements, const double* lengths,
+                          const double* coefficients, double shift, int nranks, int rank, sfem_peer* out);
+int sfem_cuda_peer_destroy(sfem_peer peer);
+/* info[8] = {x0, lx, y0, ly, x-slab elements, y-slab elements, pitch, nranks} */
+int sfem_cuda_peer_shape(sfem_peer peer, long long* info);
+/* This rank's plan-owned device buffers (x-slab, y-slab, barrier flag words). */
+int sfem_cuda_peer_buffers(sfem_peer peer, void** x_slab, void** y_slab, void** flags);
+/* Every rank's buffers as mapped in this process (own slot = own buffers;
+ * others from sfem_cuda_ipc_open_handle).  flags NULL: no device barrier
+ * (all ranks on one device, phases run rank after rank: the loopback check). */
+int sfem_cuda_peer_bind(sfem_peer peer, void* const* x_slabs, void* const* y_slabs, void* const* flags);
+int sfem_cuda_peer_phase(sfem_peer peer, int phase, void* stream);
+/* CUDA IPC of a device allocation between the ranks' processes (64-byte handles). */
+int sfem_cuda_ipc_get_handle(void* d_ptr, void* handle);
+int sfem_cuda_ipc_open_handle(const void* handle, void** d_ptr);
+int sfem_cuda_ipc_close(void* d_ptr);
+
 #ifdef __cplusplus
 }
 #endif

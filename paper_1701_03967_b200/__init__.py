@@ -91,6 +91,16 @@ _SIGS = [
     ("sfem_cuda_apply_operator", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _vp]),
     ("sfem_cuda_residual", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _dp]),
     ("sfem_cuda_max_error", ctypes.c_int, [_vp, ctypes.c_int, _dp, ctypes.c_int, _vp, ctypes.c_longlong, _dp]),
+    ("sfem_cuda_peer_create", ctypes.c_int,
+     [_vp, ctypes.c_int, _ip, _ip, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_peer_destroy", ctypes.c_int, [_vp]),
+    ("sfem_cuda_peer_shape", ctypes.c_int, [_vp, _llp]),
+    ("sfem_cuda_peer_buffers", ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    ("sfem_cuda_peer_bind", ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    ("sfem_cuda_peer_phase", ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+    ("sfem_cuda_ipc_get_handle", ctypes.c_int, [_vp, _vp]),
+    ("sfem_cuda_ipc_open_handle", ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_ipc_close", ctypes.c_int, [_vp]),
     ("sfem_cuda_dist_create", ctypes.c_int,
      [_vp, ctypes.c_int, _ip, _ip, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
     ("sfem_cuda_dist_destroy", ctypes.c_int, [_vp]),

@@ -314,6 +314,7 @@ Step strided_step(const View& v, int a, int mode) {
     s.geo.nbox = static_cast<int>((v.ext[a] + 255) / 256);
     s.geo.boxp = static_cast<int>((v.ext[a] + s.geo.nbox - 1) / s.geo.nbox);
     s.geo.nblk0 = (v.ext[N - 1] + 7) / 8;
+    s.geo.ext0 = v.ext[N - 1];
     s.geo.ext2 = static_cast<long long>(s.dims[2]);
     s.geo.ntiles = s.geo.nblk0 * static_cast<long long>(s.dims[2]) * static_cast<long long>(s.dims[3]);
   }
@@ -756,6 +757,31 @@ void apply_sweeps(sfem_plan_s* p, const double* v, double* q_out, const double* 
   }
 }
 
+// 3-D tensor map {d0 = last axis (box 8), d1 (box b), d2 (box 1)} over `base`.
+void encode_map3(CUtensorMap* m, void* base, long long e0, long long e1, long long e2, long long s1_bytes,
+                 long long s2_bytes, int box1) {
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(e0), static_cast<cuuint64_t>(e1), static_cast<cuuint64_t>(e2)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(s1_bytes), static_cast<cuuint64_t>(s2_bytes)};
+  const cuuint32_t box[3] = {8u, static_cast<cuuint32_t>(box1), 1u};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail("cuTensorMapEncodeTiled (peer map) failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// boxes of at most 256 rows, even (128-byte aligned shared-memory starts)
+void box_split(long long n, int& nbox, int& b) {
+  nbox = static_cast<int>(std::max<long long>(1, (n + 255) / 256));
+  b = static_cast<int>((n + nbox - 1) / nbox);
+  b += b & 1;
+  if (b > 256) {
+    ++nbox;
+    b = static_cast<int>((n + nbox - 1) / nbox);
+    b += b & 1;
+  }
+}
+
 double red_to_double(unsigned long long b) {
   double d;
   std::memcpy(&d, &b, sizeof d);
@@ -763,6 +789,32 @@ double red_to_double(unsigned long long b) {
 }
 
 }  // namespace
+
+// NVLink slab decomposition with the exchanges fused into the sweeps (3-D,
+// K = 64 tables on axes 0 and 1).  Rank r owns the x-slab [L1][lx_r][pitch]
+// (axis-0 rows x0_r.., laid out y, x, z) and the y-slab [ly_r][L0][pitch]
+// (axis-1 rows y0_r.., laid out y, x, z).
+struct sfem_peer_s {
+  sfem_ctx ctx = nullptr;
+  int dim = 0, nranks = 1, rank = 0;
+  std::vector<std::unique_ptr<sfem_table_s>> owned;
+  std::vector<sfem_table_s*> tables;
+  std::vector<long long> ext;
+  std::vector<double> factors;
+  double shift = 0;
+  std::vector<long long> x0, lx, y0, ly;
+  long long pitch = 0, x_elems = 0, y_elems = 0;
+  View xv, yv;
+  std::vector<Step> fwd_rows, inv_local;
+  Step fwd_y, axis0;
+  double* xbuf = nullptr;
+  double* ybuf = nullptr;
+  unsigned long long* flags = nullptr;
+  bool bound = false, device_barrier = false;
+  ScatterMaps fwd_sc{}, ax_sc{};
+  PeerFlags pf{};
+  unsigned long long epoch = 0;
+};
 
 extern "C" {
 
@@ -1459,6 +1511,207 @@ int sfem_cuda_max_error(sfem_plan p, int field, const double* params, int nparam
     ck(cudaStreamSynchronize(s), "sync");
     *error = red_to_double(h[0]);
   });
+}
+
+
+int sfem_cuda_peer_create(sfem_ctx ctx, int dim, const int* orders, const int* elements, const double* lengths,
+                          const double* coefficients, double shift, int nranks, int rank, sfem_peer* out) {
+  return guarded([&] {
+    require(ctx && orders && elements && lengths && out, "peer_create: null argument");
+    require(dim == 3, "peer_create: the fused NVLink decomposition is 3-D");
+    require(nranks >= 1 && nranks <= kMaxPeer && rank >= 0 && rank < nranks, "peer_create: bad rank / nranks");
+    validate(dim, orders, elements, lengths, coefficients, shift);
+    auto d = std::make_unique<sfem_peer_s>();
+    d->ctx = ctx;
+    d->dim = dim;
+    d->nranks = nranks;
+    d->rank = rank;
+    d->shift = shift;
+    std::map<std::pair<int, int>, sfem_table_s*> cache;
+    for (int i = 0; i < dim; ++i) {
+      const auto key = std::make_pair(orders[i], elements[i]);
+      auto it = cache.find(key);
+      if (it == cache.end()) {
+        auto t = std::make_unique<sfem_table_s>();
+        t->ctx = ctx;
+        t->host = build_host_table(orders[i], elements[i]);
+        upload_table(t.get());
+        it = cache.emplace(key, t.get()).first;
+        d->owned.push_back(std::move(t));
+      }
+      d->tables.push_back(it->second);
+      const double h = lengths[i] / elements[i];
+      d->factors.push_back((coefficients ? coefficients[i] : 1.0) * (4.0 / (h * h)));
+      d->ext.push_back(static_cast<long long>(orders[i]) * elements[i] - 1);
+    }
+    for (int i = 0; i < 2; ++i)
+      require(has_tma_sweep(d->tables[i]->dev.n, d->tables[i]->dev.K) && fast_enabled(),
+              "peer_create: axes 0 and 1 need the K = 64 TMA kernels");
+    require(d->ext[0] >= 2 * nranks && d->ext[1] >= 2 * nranks, "peer_create: fewer slab rows than ranks");
+    d->lx = balanced_even(d->ext[0], nranks, d->x0);
+    d->ly = balanced_even(d->ext[1], nranks, d->y0);
+    for (int p = 0; p < nranks; ++p) require(d->lx[p] > 0 && d->ly[p] > 0, "peer_create: empty slab");
+    d->pitch = (d->ext[2] + 3) & ~3LL;
+    const long long L0 = d->ext[0], L1 = d->ext[1], L2 = d->ext[2];
+    d->x_elems = L1 * d->lx[rank] * d->pitch;
+    d->y_elems = d->ly[rank] * L0 * d->pitch;
+    auto view = [&](long long e0, long long e1, int t0, int t1) {
+      View v;
+      v.N = 3;
+      v.ext = {e0, e1, L2};
+      v.pitch = d->pitch;
+      v.tables = {d->tables[t0], d->tables[t1], d->tables[2]};
+      v.factors = {d->factors[t0], d->factors[t1], d->factors[2]};
+      v.eig_off.assign(3, 0);
+      v.shift = shift;
+      v.use_fast = true;
+      return v;
+    };
+    d->xv = view(L1, d->lx[rank], 1, 0);  // [y][x][z]
+    d->yv = view(d->ly[rank], L0, 1, 0);  // [y][x][z]
+    d->fwd_rows.push_back(rows_step(d->xv, kForward));
+    d->fwd_y = strided_step(d->xv, 0, kForward);
+    d->axis0 = strided_step(d->yv, 1, kForward);
+    d->inv_local.push_back(strided_step(d->xv, 0, kInverse));
+    d->inv_local.push_back(rows_step(d->xv, kInverse));
+    require(d->fwd_y.tma && d->axis0.tma, "peer_create: TMA kernels unavailable");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ck(cudaMalloc(&d->xbuf, d->x_elems * sizeof(double)), "cudaMalloc(x-slab)");
+    ck(cudaMalloc(&d->ybuf, d->y_elems * sizeof(double)), "cudaMalloc(y-slab)");
+    ck(cudaMalloc(&d->flags, kMaxPeer * sizeof(unsigned long long)), "cudaMalloc(flags)");
+    ck(cudaMemset(d->xbuf, 0, d->x_elems * sizeof(double)), "memset");
+    ck(cudaMemset(d->ybuf, 0, d->y_elems * sizeof(double)), "memset");
+    ck(cudaMemset(d->flags, 0, kMaxPeer * sizeof(unsigned long long)), "memset");
+    *out = d.release();
+  });
+}
+
+int sfem_cuda_peer_destroy(sfem_peer d) {
+  return guarded([&] {
+    if (!d) return;
+    cudaSetDevice(d->ctx->device);
+    if (d->xbuf) cudaFree(d->xbuf);
+    if (d->ybuf) cudaFree(d->ybuf);
+    if (d->flags) cudaFree(d->flags);
+    for (auto& t : d->owned)
+      if (t->dbuf) cudaFree(t->dbuf);
+    delete d;
+  });
+}
+
+int sfem_cuda_peer_shape(sfem_peer d, long long* info) {
+  return guarded([&] {
+    require(d && info, "peer_shape: null argument");
+    const int r = d->rank;
+    const long long v[8] = {d->x0[r], d->lx[r], d->y0[r], d->ly[r], d->x_elems, d->y_elems, d->pitch, d->nranks};
+    std::copy(v, v + 8, info);
+  });
+}
+
+int sfem_cuda_peer_buffers(sfem_peer d, void** x_slab, void** y_slab, void** flags) {
+  return guarded([&] {
+    require(d != nullptr, "peer_buffers: null plan");
+    if (x_slab) *x_slab = d->xbuf;
+    if (y_slab) *y_slab = d->ybuf;
+    if (flags) *flags = d->flags;
+  });
+}
+
+int sfem_cuda_peer_bind(sfem_peer d, void* const* x_slabs, void* const* y_slabs, void* const* flags) {
+  return guarded([&] {
+    require(d && x_slabs && y_slabs, "peer_bind: null argument");
+    const int P = d->nranks, r = d->rank;
+    const long long L0 = d->ext[0], L1 = d->ext[1], L2 = d->ext[2], pitch = d->pitch;
+    require(x_slabs[r] == d->xbuf && y_slabs[r] == d->ybuf, "peer_bind: own slot must hold this rank's slabs");
+    // forward exchange: tile rows y0_q.. of the axis-1 sweep -> rank q's y-slab
+    // viewed {z, y_local, x}: box {8, b, 1} at (c0, j b, x0_r + x_local)
+    ScatterMaps& f = d->fwd_sc;
+    f.npeer = P;
+    f.fbase = d->x0[r];
+    for (int q = 0; q < P; ++q) {
+      f.r0[q] = static_cast<int>(d->y0[q]);
+      f.n[q] = static_cast<int>(d->ly[q]);
+      box_split(d->ly[q], f.nbox[q], f.b[q]);
+      encode_map3(&f.map[q], y_slabs[q], L2, d->ly[q], L0, L0 * pitch * 8, pitch * 8, f.b[q]);
+    }
+    // return exchange: tile rows x0_p.. of the axis-0 sweep -> rank p's x-slab
+    // viewed {z, x_local, y}: box {8, b, 1} at (c0, j b, y0_r + y_local)
+    ScatterMaps& a = d->ax_sc;
+    a.npeer = P;
+    a.fbase = d->y0[r];
+    for (int p = 0; p < P; ++p) {
+      a.r0[p] = static_cast<int>(d->x0[p]);
+      a.n[p] = static_cast<int>(d->lx[p]);
+      box_split(d->lx[p], a.nbox[p], a.b[p]);
+      encode_map3(&a.map[p], x_slabs[p], L2, d->lx[p], L1, pitch * 8, d->lx[p] * pitch * 8, a.b[p]);
+    }
+    d->device_barrier = flags != nullptr;
+    if (flags)
+      for (int q = 0; q < P; ++q) d->pf.f[q] = static_cast<unsigned long long*>(flags[q]);
+    encode_map(d->fwd_y, d->xbuf);
+    encode_map(d->axis0, d->ybuf);
+    d->bound = true;
+  });
+}
+
+int sfem_cuda_peer_phase(sfem_peer d, int phase, void* stream) {
+  return guarded([&] {
+    require(d != nullptr, "peer_phase: null plan");
+    require(d->bound, "peer_phase: peers not bound (sfem_cuda_peer_bind)");
+    ck(cudaSetDevice(d->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    const PeerDivide none{};
+    switch (phase) {
+      case SFEM_PEER_FORWARD:
+        launch_steps(d->fwd_rows, d->xbuf, d->ctx, s, nullptr);
+        ck(launch_sweep_tma_scatter(d->tables[1]->dev, &d->fwd_y.map, d->fwd_y.geo, kForward, d->fwd_sc, none, s),
+           "peer forward exchange sweep");
+        break;
+      case SFEM_PEER_AXIS0: {
+        PeerDivide dv{};
+        dv.shift = d->shift;
+        dv.f1 = d->factors[1];
+        dv.f2 = d->factors[2];
+        dv.f_last = d->factors[0];
+        dv.eig1 = d->tables[1]->dev.eig + d->y0[d->rank];
+        dv.eig2 = d->tables[2]->dev.eig;
+        ck(launch_sweep_tma_scatter(d->tables[0]->dev, &d->axis0.map, d->axis0.geo, kForwardDivideInverse, d->ax_sc,
+                                    dv, s),
+           "peer axis-0 exchange sweep");
+        break;
+      }
+      case SFEM_PEER_INVERSE:
+        launch_steps(d->inv_local, d->xbuf, d->ctx, s, nullptr);
+        break;
+      case SFEM_PEER_BARRIER:
+        if (d->device_barrier) ck(launch_peer_barrier(d->pf, d->nranks, d->rank, ++d->epoch, s), "peer barrier");
+        break;
+      default:
+        fail("peer_phase: unknown phase");
+    }
+  });
+}
+
+int sfem_cuda_ipc_get_handle(void* d_ptr, void* handle) {
+  return guarded([&] {
+    require(d_ptr && handle, "ipc_get_handle: null argument");
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, d_ptr), "cudaIpcGetMemHandle");
+    std::memcpy(handle, &h, sizeof h);
+  });
+}
+
+int sfem_cuda_ipc_open_handle(const void* handle, void** d_ptr) {
+  return guarded([&] {
+    require(d_ptr && handle, "ipc_open_handle: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    ck(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+int sfem_cuda_ipc_close(void* d_ptr) {
+  return guarded([&] { ck(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle"); });
 }
 
 }  // extern "C"

@@ -2,6 +2,7 @@
 // orchestrator (capi.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sfem_b200 {
@@ -65,6 +66,7 @@ enum SweepMode { kForward = 0, kInverse = 1, kForwardDivideInverse = 2 };
 struct TmaGeom {
   int nbox, boxp;      // boxes along d1 (boxp positions each, nbox*boxp >= L)
   long long nblk0;     // ceil(L_d0 / 8)
+  long long ext0;      // L_d0 (extent of the last axis)
   long long ext2;      // extent of d2
   long long ntiles;    // nblk0 * ext2 * ext3
 };
@@ -89,6 +91,38 @@ struct RowSegs {
   long long off[kMaxSeg], stride[kMaxSeg];
 };
 bool has_bulk_rows(int n, int K);
+
+// Strided TMA sweep whose tile stores go to other ranks' tensors (NVLink peer
+// memory; local buffers in the single-device loopback): peer q receives tile
+// rows [r0[q], r0[q] + n[q]) through map[q], a 3-D tensor map {last axis,
+// target rows, fixed} with box {8, b[q], 1}, at coordinates
+// (c0, j * b[q], fbase + c2) for boxes j < nbox[q] (c0: the tile's first
+// last-axis index, c2: the tile's fixed coordinate of the load geometry).
+// MODE kForward (axis-1 forward on the x-slab) or kForwardDivideInverse (the
+// axis-0 sweep on the y-slab, divide base = (shift + f1 eig1[c2]) + f2 eig2[z],
+// then + f_last eig[pos] of the swept table).
+constexpr int kMaxPeer = 8;
+struct alignas(64) ScatterMaps {
+  CUtensorMap map[kMaxPeer];
+  int npeer;
+  long long fbase;
+  int r0[kMaxPeer], n[kMaxPeer], b[kMaxPeer], nbox[kMaxPeer];
+};
+struct PeerDivide {
+  double shift, f1, f2, f_last;
+  const double* eig1;  // already offset to the rank's first row
+  const double* eig2;
+};
+cudaError_t launch_sweep_tma_scatter(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode,
+                                     const ScatterMaps& sc, const PeerDivide& dv, cudaStream_t stream);
+// Device barrier among ranks over peer-mapped flag words: rank `rank` writes
+// `epoch` into flags[q][rank] of every q and waits until its own
+// flags[rank][0..nranks) all reach `epoch` (system-scope release / acquire).
+struct PeerFlags {
+  unsigned long long* f[kMaxPeer];
+};
+cudaError_t launch_peer_barrier(const PeerFlags& fl, int nranks, int rank, unsigned long long epoch,
+                                cudaStream_t stream);
 cudaError_t launch_sweep_bulk_rows(const DevTable& t, double* data, const RowSegs& segs, long long nrows, int mode,
                                    int analysis, const SymbolInfo& sym, cudaStream_t stream);
 enum AnalysisKind { kWeighted = 0, kDirect = 1 };

@@ -203,3 +203,147 @@ def gather_x(plan: DistPlan, x) -> np.ndarray:
     ext = plan.extents
     rows = x.view(-1, plan.xpitch)[:, :ext[-1]].cpu().numpy()
     return rows.reshape([plan.lx] + list(ext[1:]))
+
+
+# ---------------------------------------------------------------------------
+# Fused NVLink exchange (sfem_cuda_peer_*): the all-to-all transposes travel
+# inside the axis-1 forward and axis-0 sweeps as TMA stores into the other
+# ranks' slabs (peer memory); no collective on the data path.
+# ---------------------------------------------------------------------------
+PEER_FORWARD, PEER_AXIS0, PEER_INVERSE, PEER_BARRIER = 0, 1, 2, 3
+
+
+class PeerPlan:
+    """One rank's share of the fused NVLink solve (3-D, K = 64 on axes 0, 1).
+    Buffers are plan-owned: x-slab [L1][lx][pitch] (laid out y, x, z), y-slab
+    [ly][L0][pitch]."""
+
+    def __init__(self, spec: ProblemSpec, nranks: int, rank: int, ctx: Optional[Context] = None):
+        spec.validate()
+        self.ctx = ctx or default_context()
+        self.spec = spec
+        N = spec.dimension
+        h = _vp()
+        coeffs = (ctypes.c_double * N)(*spec.coefficients) if spec.coefficients is not None else None
+        _check(lib.sfem_cuda_peer_create(self.ctx.handle, N, (ctypes.c_int * N)(*spec.orders),
+                                         (ctypes.c_int * N)(*spec.elements), (ctypes.c_double * N)(*spec.lengths),
+                                         ctypes.cast(coeffs, _dp) if coeffs is not None else None,
+                                         float(spec.shift), nranks, rank, ctypes.byref(h)))
+        self.handle = h
+        info = (ctypes.c_longlong * 8)()
+        _check(lib.sfem_cuda_peer_shape(h, info))
+        self.x0, self.lx, self.y0, self.ly, self.x_elems, self.y_elems, self.pitch, _ = list(info)
+        xp, yp, fp = _vp(), _vp(), _vp()
+        _check(lib.sfem_cuda_peer_buffers(h, ctypes.byref(xp), ctypes.byref(yp), ctypes.byref(fp)))
+        self.x_ptr, self.y_ptr, self.flags_ptr = xp.value, yp.value, fp.value
+        self.nranks, self.rank = nranks, rank
+        self.extents = spec.extents()
+        self._opened = []
+
+    def bind(self, x_ptrs, y_ptrs, flag_ptrs=None):
+        P = self.nranks
+        arr = lambda v: (_vp * P)(*[_vp(int(x)) for x in v])  # noqa: E731
+        _check(lib.sfem_cuda_peer_bind(self.handle, arr(x_ptrs), arr(y_ptrs),
+                                       arr(flag_ptrs) if flag_ptrs is not None else None))
+
+    def phase(self, ph: int, stream: int = 0):
+        _check(lib.sfem_cuda_peer_phase(self.handle, ph, _vp(stream or None)))
+
+    def solve(self, stream: int = 0):
+        """One solve (the bound ranks run their phases concurrently on their
+        own devices; the device barriers order the exchanges)."""
+        for ph in (PEER_FORWARD, PEER_BARRIER, PEER_AXIS0, PEER_BARRIER, PEER_INVERSE):
+            self.phase(ph, stream)
+
+    # ---- slab data (dense global dof tensor <-> this rank's x-slab) ----
+    def x_view(self):
+        """torch view of the plan-owned x-slab [L1][lx][pitch]."""
+        return _wrap_device(self.x_ptr, (self.extents[1], self.lx, self.pitch), self.ctx.device)
+
+    def scatter_x(self, load: np.ndarray):
+        import torch
+        v = self.x_view()
+        blk = np.ascontiguousarray(np.transpose(load[self.x0:self.x0 + self.lx], (1, 0, 2)))
+        v[:, :, :self.extents[2]].copy_(torch.from_numpy(blk))
+
+    def gather_x(self) -> np.ndarray:
+        import torch
+        torch.cuda.synchronize(self.ctx.device)
+        blk = self.x_view()[:, :, :self.extents[2]].cpu().numpy()
+        return np.ascontiguousarray(np.transpose(blk, (1, 0, 2)))
+
+    def close(self):
+        for ptr in self._opened:
+            lib.sfem_cuda_ipc_close(_vp(ptr))
+        self._opened = []
+        if self.handle:
+            lib.sfem_cuda_peer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _wrap_device(ptr: int, shape, device: int):
+    """A torch view of plan-owned device memory (no copy, no ownership)."""
+    import torch
+
+    class _Arr:
+        def __init__(self):
+            strides = []
+            acc = 1
+            for d in reversed(shape):
+                strides.append(acc * 8)
+                acc *= d
+            self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (int(ptr), False),
+                                             "version": 2, "strides": tuple(reversed(strides))}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Arr(), device=f"cuda:{device}")
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib.sfem_cuda_ipc_get_handle(_vp(ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    out = _vp()
+    buf = ctypes.create_string_buffer(handle, 64)
+    _check(lib.sfem_cuda_ipc_open_handle(buf, ctypes.byref(out)))
+    return out.value
+
+
+def peer_bind_distributed(plan: PeerPlan, dist_mod) -> None:
+    """Exchange the ranks' buffer handles over torch.distributed and bind the
+    peers (one process per GPU, NVLink P2P)."""
+    mine = [ipc_handle(plan.x_ptr), ipc_handle(plan.y_ptr), ipc_handle(plan.flags_ptr)]
+    allh = [None] * plan.nranks
+    dist_mod.all_gather_object(allh, mine)
+    xs, ys, fs = [], [], []
+    for q, hs in enumerate(allh):
+        if q == plan.rank:
+            xs.append(plan.x_ptr), ys.append(plan.y_ptr), fs.append(plan.flags_ptr)
+            continue
+        ptrs = [ipc_open(h) for h in hs]
+        plan._opened += ptrs
+        xs.append(ptrs[0]), ys.append(ptrs[1]), fs.append(ptrs[2])
+    plan.bind(xs, ys, fs)
+
+
+def peer_solve_loopback(plans: Sequence[PeerPlan], stream: int = 0) -> None:
+    """All ranks on one device (the single-GPU check): phases rank after rank,
+    no device barrier (stream order is the barrier)."""
+    for ph in (PEER_FORWARD, PEER_AXIS0, PEER_INVERSE):
+        for p in plans:
+            p.phase(ph, stream)
+
+
+def peer_bind_loopback(plans: Sequence[PeerPlan]) -> None:
+    xs = [p.x_ptr for p in plans]
+    ys = [p.y_ptr for p in plans]
+    for p in plans:
+        p.bind(xs, ys, None)

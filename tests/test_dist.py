@@ -184,3 +184,63 @@ def test_loopback_slab_solve_matches_single_gpu(sfem, P, orders, elements, lengt
     torch.cuda.synchronize()
     got = np.concatenate([D.gather_x(p, b[0]) for p, b in zip(plans, bufs)], axis=0)
     assert rel_l2(got, want) <= 1e-13
+
+
+# ---- fused NVLink exchange (sfem_cuda_peer_*), loopback on one GPU ---------
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("orders,elements,shift", [
+    ([2, 3, 4], [64, 64, 7], 0.5),      # odd L0 = 127, L1 = 191: uneven slabs, pad rows
+    ([9, 5, 9], [64, 64, 3], 0.0),      # n = 9 axis-0 fused sweep, short rows
+])
+def test_peer_exchange_loopback_matches_single_gpu(P, orders, elements, shift):
+    import paper_1701_03967_b200 as sfem
+    from paper_1701_03967_b200 import dist as D
+    spec = sfem.ProblemSpec(3, [1.0, 1.3, 0.7], elements, orders, shift)
+    f = np.random.default_rng(P).uniform(-1, 1, spec.extents())
+    want, _ = sfem.solve_dof(spec, f)
+    plans = [D.PeerPlan(spec, P, r) for r in range(P)]
+    D.peer_bind_loopback(plans)
+    for p in plans:
+        p.scatter_x(f)
+    D.peer_solve_loopback(plans)
+    got = np.concatenate([p.gather_x() for p in plans], axis=0)
+    assert rel_l2(got, want) <= 1e-13
+    # a second solve on the same plans (buffers reused)
+    for p in plans:
+        p.scatter_x(f)
+    D.peer_solve_loopback(plans)
+    got2 = np.concatenate([p.gather_x() for p in plans], axis=0)
+    assert np.array_equal(got, got2)
+    for p in plans:
+        p.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_peer_exchange_loopback_config4_p8():
+    import paper_1701_03967_b200 as sfem
+    from paper_1701_03967_b200 import dist as D
+    spec = sfem.ProblemSpec(3, [1.0] * 3, [64] * 3, [9] * 3, 0.0)
+    f = np.random.default_rng(4).uniform(-1, 1, spec.extents())
+    want, _ = sfem.solve_dof(spec, f)
+    plans = [D.PeerPlan(spec, 8, r) for r in range(8)]
+    D.peer_bind_loopback(plans)
+    for p in plans:
+        p.scatter_x(f)
+    D.peer_solve_loopback(plans)
+    got = np.concatenate([p.gather_x() for p in plans], axis=0)
+    assert rel_l2(got, want) <= 1e-13
+    for p in plans:
+        p.close()
+
+
+def test_peer_partition_host_logic():
+    # both slab axes split into even-start pieces (128-byte aligned TMA boxes)
+    from paper_1701_03967_b200.dist import partition_even
+    for n in (127, 191, 575, 1023):
+        for P in range(1, 9):
+            offs, lens = partition_even(n, P)
+            assert sum(lens) == n and all(o % 2 == 0 for o in offs)
+            assert max(lens) - min(lens) <= 3
