@@ -11,8 +11,12 @@ no flush is needed between steps).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4|...]
 
-N > 1 (torchrun, one rank per GPU, NCCL): each rank solves its own C4 problem
-("scaling": "weak"); value = total unknowns / max-over-ranks time.
+N > 1 (torchrun, one rank per GPU): ONE global problem, slab-decomposed along
+axis 0 ("scaling": "strong"); value = global unknowns / max-over-ranks time.
+Default --dist-mode peer: the two transposes are fused into the sweeps as TMA
+stores into the other ranks' slabs over NVLink (CUDA IPC), device flag
+barriers between phases; --dist-mode nccl: NCCL all-to-all between the
+sweeps.  If both fail the ranks fall back to independent replicas.
 """
 import argparse
 import json
@@ -182,6 +186,100 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def peer_capable(config):
+    orders, elements = CONFIGS[config][0], CONFIGS[config][1]
+    return len(orders) == 3 and elements[0] == 64 and elements[1] == 64 and orders[0] in (2, 3, 4, 5, 9) \
+        and orders[1] in (2, 3, 4, 5, 9)
+
+
+def run_peer(args, world, rank, local, dist):
+    """N > 1, fused NVLink exchange: ONE global problem in
+    axis-0 slabs; the axis-1 forward sweep and the axis-0 sweep store their
+    tiles straight into the other ranks' slabs (CUDA IPC peer memory), a
+    device flag barrier between the phases; no collective on the data path.
+    Strong scaling: value = global unknowns / max-over-ranks time."""
+    import torch
+    import paper_1701_03967_b200 as sfem
+    from paper_1701_03967_b200 import dist as D
+
+    orders, elements, lengths, coeffs, shift, desc = CONFIGS[args.config]
+    spec = sfem.ProblemSpec(len(orders), lengths, elements, orders, shift, coefficients=coeffs)
+    ctx = sfem.Context(local)
+    plan = D.PeerPlan(spec, world, rank, ctx)
+    D.peer_bind_distributed(plan, dist)
+    U = int(np.prod(plan.extents))
+    ext = torch.cuda.ExternalStream(ctx.stream)
+    xv = plan.x_view()
+    L1, L2 = plan.extents[1], plan.extents[2]
+    f_local = np.random.default_rng(1000 + rank).uniform(-1.0, 1.0, (L1, plan.lx, L2))
+    xv[:, :, :L2].copy_(torch.from_numpy(f_local))
+    torch.cuda.synchronize()
+    barrier(dist, world)
+
+    def solve():
+        plan.solve(ctx.stream)
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    barrier(dist, world)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        barrier(dist, world)
+        ev0.record(ext)
+        for _ in range(args.steps):
+            solve()
+        ev1.record(ext)
+        torch.cuda.synchronize()
+    barrier(dist, world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), dist, world)
+    value = U * args.steps / (ms * 1e-3)
+    ms_step = ms / args.steps
+    peaks, peak_kind = measured_peaks()
+    local_u = U / world
+    hbm_bytes = 16.0 * local_u * 5  # five sweeps, each reads and writes the rank's share once
+    achieved = hbm_bytes / (ms_step * 1e-3) / 1e9
+    nvl_bytes = 2 * 8.0 * local_u * (world - 1) / world
+
+    h_in = torch.from_numpy(f_local).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    barrier(dist, world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        with torch.cuda.stream(ext):
+            xv[:, :, :L2].copy_(h_in, non_blocking=True)
+        solve()
+        with torch.cuda.stream(ext):
+            h_out.copy_(xv[:, :, :L2], non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, dist, world)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "unknowns": U, "extents": plan.extents,
+                       "parallelism": f"slab x{world} (axis-0 slabs; exchanges fused into the sweeps as TMA "
+                                      "stores to NVLink peer memory)",
+                       "l2_flush": "none needed: tensors > L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "whole per-rank solve (5 sweeps, 2 of them storing to peers)",
+                         "nvlink_bytes_per_rank_per_solve": nvl_bytes},
+            "cpu_baseline": None,
+            "e2e": {"value": U / e2e_s, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * int(f_local.size) * world,
+                    "d2h_bytes_per_step": 8 * int(f_local.size) * world, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": 7 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+
+
 def run_distributed(args, world, rank, local, dist):
     """N > 1: ONE global problem, slab-decomposed over the ranks (axis-0 slabs,
     two NCCL all-to-all transposes per solve; paper_1701_03967_b200/dist.py).
@@ -275,6 +373,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-mode", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: exchanges fused into the sweeps over NVLink peer memory, or NCCL all-to-all")
     ap.add_argument("--dist-single", action="store_true",
                     help="exercise the slab-decomposed path on one GPU (1-rank NCCL group)")
     args = ap.parse_args()
@@ -290,7 +390,10 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29555")
         torch.cuda.set_device(0)
         tdist.init_process_group("nccl", rank=0, world_size=1)
-        run_distributed(args, 1, 0, 0, tdist)
+        if args.dist_mode == "peer" and peer_capable(args.config):
+            run_peer(args, 1, 0, 0, tdist)
+        else:
+            run_distributed(args, 1, 0, 0, tdist)
         tdist.destroy_process_group()
         return
     if args.impl == "reference":
@@ -303,6 +406,19 @@ def main():
     import paper_1701_03967_b200 as sfem
 
     torch.cuda.set_device(local)
+    if world > 1 and args.dist_mode == "peer" and peer_capable(args.config):
+        ok = True
+        try:
+            run_peer(args, world, rank, local, dist)
+        except Exception as e:
+            ok = False
+            print(f"[bench] fused NVLink solve failed on rank {rank}: {e!r}; NCCL slab path next", file=sys.stderr)
+            args.dist_error = repr(e)
+        flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if flag.item() == 1.0:
+            dist.destroy_process_group()
+            return
     if world > 1:
         try:
             run_distributed(args, world, rank, local, dist)

@@ -244,3 +244,57 @@ def test_peer_partition_host_logic():
             offs, lens = partition_even(n, P)
             assert sum(lens) == n and all(o % 2 == 0 for o in offs)
             assert max(lens) - min(lens) <= 3
+
+
+def _peer_bind_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1701_03967_b200 import dist as D
+
+        class FakePlan:  # host-side view of PeerPlan (no device)
+            def __init__(self):
+                self.rank, self.nranks = rank, world
+                self.x_ptr, self.y_ptr, self.flags_ptr = 1000 * (rank + 1) + 1, 1000 * (rank + 1) + 2, \
+                    1000 * (rank + 1) + 3
+                self._opened = []
+                self.bound = None
+
+            def bind(self, xs, ys, fs):
+                self.bound = (list(xs), list(ys), list(fs))
+
+        opened = {}
+        D_ipc_handle, D_ipc_open = D.ipc_handle, D.ipc_open
+        D.ipc_handle = lambda ptr: ptr.to_bytes(8, "little") * 8
+        D.ipc_open = lambda h: opened.setdefault(h, 10 ** 6 + int.from_bytes(h[:8], "little"))
+        try:
+            p = FakePlan()
+            D.peer_bind_distributed(p, dist)
+        finally:
+            D.ipc_handle, D.ipc_open = D_ipc_handle, D_ipc_open
+        q.put((rank, p.bound, sorted(p._opened)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_bind_exchanges_handles_gloo(world):
+    # every rank binds its own buffers in its own slot and the opened peer
+    # buffers (from the other ranks' handles) in the others, in rank order
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_bind_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict((r, (b, o)) for r, b, o in (q.get(timeout=120) for _ in range(world)))
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in range(world):
+        (xs, ys, fs), opened = res[r]
+        for qq in range(world):
+            base = 1000 * (qq + 1)
+            off = 0 if qq == r else 10 ** 6
+            assert xs[qq] == off + base + 1 and ys[qq] == off + base + 2 and fs[qq] == off + base + 3
+        assert len(opened) == 3 * (world - 1)
