@@ -288,6 +288,58 @@ struct SolveReport {
   std::optional<double> error_uniform;
 };
 
+// A built-in right-hand side: the device stand-in for ProblemSpec::rhs /
+// exact (poisson.hpp:39-40), see sfem_cuda_fem_load.
+struct Field {
+  int kind = SFEM_FIELD_CONSTANT;
+  std::vector<double> params{1.0};
+  static Field constant(double v) { return Field{SFEM_FIELD_CONSTANT, {v}}; }
+  static Field sines(double amp, const std::vector<double>& k) {
+    Field f{SFEM_FIELD_SINES, {amp}};
+    f.params.insert(f.params.end(), k.begin(), k.end());
+    return f;
+  }
+  // the reference's manufactured cases by name (cases.cpp:61-78)
+  static Field manufactured(const std::string& name) {
+    if (name == "sin1d") return Field{SFEM_FIELD_SIN1D, {}};
+    if (name == "poisson2d") return Field{SFEM_FIELD_POISSON2D, {}};
+    if (name == "poisson3d") return Field{SFEM_FIELD_POISSON3D, {}};
+    if (name == "constant1d" || name == "constant2d" || name == "constant3d") return constant(1.0);
+    fail("unknown case '" + name + "' (known: sin1d, poisson2d, poisson3d, constant1d, constant2d, constant3d)");
+  }
+};
+
+// dense dof tensor <-> 2^N class arrays (per axis: dof t with t % n == n-1 is
+// node (t+1)/n, else interior index (t/n)*(n-1) + t%n; ndgrid.hpp:43-57)
+inline GridFunctionND classes_from_dof(const std::vector<AxisSpec>& axes, const std::vector<double>& dof) {
+  GridFunctionND g = GridFunctionND::zeros(axes);
+  const int N = static_cast<int>(axes.size());
+  std::vector<long long> ext(N);
+  for (int i = 0; i < N; ++i) ext[i] = static_cast<long long>(axes[i].order) * axes[i].elements - 1;
+  std::vector<long long> t(N, 0);
+  for (size_t flat = 0; flat < dof.size(); ++flat) {
+    unsigned mask = 0;
+    long long off = 0;
+    for (int i = 0; i < N; ++i) {
+      const int n = axes[i].order;
+      const bool node = t[i] % n == n - 1;
+      if (!node) mask |= 1u << i;
+    }
+    const std::vector<int> cext = g.class_extents(mask);
+    for (int i = 0; i < N; ++i) {
+      const int n = axes[i].order;
+      const long long idx = (t[i] % n == n - 1) ? (t[i] + 1) / n : (t[i] / n) * (n - 1) + t[i] % n;
+      off = off * cext[i] + idx;
+    }
+    g.classes[mask][static_cast<size_t>(off)] = dof[flat];
+    for (int i = N - 1; i >= 0; --i) {
+      if (++t[i] < ext[i]) break;
+      t[i] = 0;
+    }
+  }
+  return g;
+}
+
 // A device plan for one ProblemSpec (sfem_cuda_plan_create).
 class Plan {
  public:
@@ -306,6 +358,27 @@ class Plan {
     double sec = 0;
     check(sfem_cuda_solve_host(h_, load, u, &sec));
     return sec;
+  }
+  long long unknowns() const {
+    long long u = 0;
+    check(sfem_cuda_plan_shape(h_, nullptr, nullptr, &u));
+    return u;
+  }
+  // y = A v on dense dof tensors (apply_operator, poisson.cpp:749-769)
+  void apply_operator_dof(const double* v, double* y) { check(sfem_cuda_apply_operator_host(h_, v, y)); }
+  // the reference's solve(spec, options) of a field, every step on the device
+  SolveReport solve_field(const Field& f, bool compute_residual) {
+    std::vector<double> u(static_cast<size_t>(unknowns()));
+    double rep[4];
+    check(sfem_cuda_solve_field(h_, f.kind, f.params.empty() ? nullptr : f.params.data(),
+                                static_cast<int>(f.params.size()), compute_residual ? 1 : 0, u.data(), rep));
+    SolveReport r;
+    r.solution = classes_from_dof(spec_.axis_specs(), u);
+    r.seconds_load = rep[0];
+    r.seconds_solve = rep[1];
+    if (!std::isnan(rep[2])) r.residual_rel = rep[2];
+    if (!std::isnan(rep[3])) r.error_uniform = rep[3];
+    return r;
   }
   GridFunctionND solve_classes(const GridFunctionND& load, double* seconds) {
     GridFunctionND out = GridFunctionND::zeros(spec_.axis_specs());
@@ -335,6 +408,18 @@ inline SolveReport solve_with_load(const ProblemSpec& spec, const GridFunctionND
   SolveReport r;
   r.solution = plan.solve_classes(load, &r.seconds_solve);
   return r;
+}
+
+// solve (poisson.hpp:86; poisson.cpp:796-808): FEM load of `rhs`, the solve,
+// and on request the residual check / uniform error, all on the GPU.
+inline SolveReport solve(const ProblemSpec& spec, const Field& rhs, const SolveOptions& options = {}) {
+  spec.validate();
+  if (options.algorithm != Algorithm::FullDiagonalization)
+    fail("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path");
+  static TableSet local;
+  TableSet& tables = options.tables ? *options.tables : local;
+  Plan plan(tables.context(), spec);
+  return plan.solve_field(rhs, options.compute_residual);
 }
 
 }  // namespace sfem_b200

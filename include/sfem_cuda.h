@@ -144,6 +144,17 @@ int sfem_cuda_residual(sfem_plan plan, const double* d_u, const double* d_f, lon
 int sfem_cuda_max_error(sfem_plan plan, int field, const double* params, int nparams, const double* d_u,
                         long long pitch, double* error);
 
+/* The reference's end-to-end solve(spec, options) (poisson.cpp:796-808) of a
+ * built-in field, every step on the device: FEM load, solve, optionally the
+ * residual check, and the uniform error for fields with a known solution.
+ * report[4] = {seconds_load, seconds_solve, residual_rel (NaN unless
+ * compute_residual), error_uniform (NaN for CONSTANT)}; h_u (dense dof
+ * layout, may be NULL) receives the solution. */
+int sfem_cuda_solve_field(sfem_plan plan, int field, const double* params, int nparams, int compute_residual,
+                          double* h_u, double* report);
+/* apply_operator (poisson.cpp:749-769) on dense host dof tensors. */
+int sfem_cuda_apply_operator_host(sfem_plan plan, const double* h_v, double* h_y);
+
 /* ---- Multi-GPU slab decomposition (one process / context per GPU) ----
  * Rank r owns the x-slab of axis-0 dof rows [x0, x0+lx) of the global dof
  * tensor (all other axes; last axis padded to xpitch) and, between the two

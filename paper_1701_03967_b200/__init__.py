@@ -91,6 +91,8 @@ _SIGS = [
     ("sfem_cuda_apply_operator", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _vp]),
     ("sfem_cuda_residual", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _dp]),
     ("sfem_cuda_max_error", ctypes.c_int, [_vp, ctypes.c_int, _dp, ctypes.c_int, _vp, ctypes.c_longlong, _dp]),
+    ("sfem_cuda_solve_field", ctypes.c_int, [_vp, ctypes.c_int, _dp, ctypes.c_int, ctypes.c_int, _dp, _dp]),
+    ("sfem_cuda_apply_operator_host", ctypes.c_int, [_vp, _dp, _dp]),
     ("sfem_cuda_peer_create", ctypes.c_int,
      [_vp, ctypes.c_int, _ip, _ip, _dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
     ("sfem_cuda_peer_destroy", ctypes.c_int, [_vp]),
@@ -477,6 +479,26 @@ class Plan:
                                        self.pitch if pitch is None else pitch, ctypes.byref(e)))
         return e.value
 
+    def apply_operator_host(self, v: np.ndarray) -> np.ndarray:
+        """sfem_cuda_apply_operator_host: A v on a dense host dof tensor."""
+        v = _f64(v)
+        if list(v.shape) != self.extents:
+            raise Error(f"apply_operator: shape {list(v.shape)} does not match the dof extents {self.extents}")
+        y = np.empty_like(v)
+        _check(lib.sfem_cuda_apply_operator_host(self.handle, _dptr(v), _dptr(y)))
+        return y
+
+    def solve_field(self, field: "Field", compute_residual: bool = False) -> "SolveReport":
+        """sfem_cuda_solve_field: the reference's solve(spec, options) on the device."""
+        prm = _f64(field.params if len(field.params) else [0.0])
+        u = np.empty(self.extents)
+        rep = np.zeros(4)
+        _check(lib.sfem_cuda_solve_field(self.handle, field.kind, _dptr(prm), len(field.params),
+                                         int(compute_residual), _dptr(u), _dptr(rep)))
+        return SolveReport(solution=u, seconds_load=float(rep[0]), seconds_solve=float(rep[1]),
+                           residual_rel=None if np.isnan(rep[2]) else float(rep[2]),
+                           error_uniform=None if np.isnan(rep[3]) else float(rep[3]))
+
     def solve_classes(self, load: GridFunctionND) -> GridFunctionND:
         N = self.spec.dimension
         ins = [_f64(c) for c in load.classes]
@@ -548,13 +570,6 @@ class Field:
         return self.kind != FIELD_CONSTANT
 
 
-def _torch():
-    import torch  # device memory / events only (plumbing)
-    if not torch.cuda.is_available():
-        raise Error("solve: no CUDA device")
-    return torch
-
-
 def solve(spec: ProblemSpec, rhs: Field, options: Optional[SolveOptions] = None,
           ctx: Optional[Context] = None) -> SolveReport:
     """solve (poisson.hpp:86; poisson.cpp:796-808) with every step on the device:
@@ -564,28 +579,4 @@ def solve(spec: ProblemSpec, rhs: Field, options: Optional[SolveOptions] = None,
     options = options or SolveOptions()
     if options.algorithm != "full":
         raise Error("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path")
-    torch = _torch()
-    plan = Plan(spec, ctx)
-    dev = torch.device("cuda", plan.ctx.device)
-    f = torch.empty(plan.padded_shape, dtype=torch.float64, device=dev)
-    u = torch.empty_like(f)
-    s = torch.cuda.ExternalStream(plan.ctx.stream, device=dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    torch.cuda.synchronize(dev)
-    with torch.cuda.stream(s):
-        ev[0].record(s)
-        plan.fem_load_device(rhs, f.data_ptr())
-        ev[1].record(s)
-        u.copy_(f)
-        ev[2].record(s)
-        plan.solve_device(u.data_ptr())
-        ev[3].record(s)
-    s.synchronize()
-    rep = SolveReport(solution=u[..., :plan.extents[-1]].cpu().numpy().copy(),
-                      seconds_load=ev[0].elapsed_time(ev[1]) / 1e3,
-                      seconds_solve=ev[2].elapsed_time(ev[3]) / 1e3)
-    if options.compute_residual:
-        rep.residual_rel = plan.residual_device(u.data_ptr(), f.data_ptr())
-    if rhs.has_exact:
-        rep.error_uniform = plan.max_error_device(rhs, u.data_ptr())
-    return rep
+    return Plan(spec, ctx).solve_field(rhs, options.compute_residual)

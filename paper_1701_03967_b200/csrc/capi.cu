@@ -421,6 +421,7 @@ struct sfem_plan_s {
   // operator / residual scratch (P and Q tensors, padded) and reduction slots
   double* opwork[2] = {nullptr, nullptr};
   unsigned long long* dred = nullptr;
+  double* fbuf = nullptr;      // device load of sfem_cuda_solve_field / operator output
   double* load_vec = nullptr;  // per-axis 1-D loads of separable fields
   size_t load_vec_cap = 0;
 };
@@ -1019,6 +1020,7 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
       if (w) cudaFree(w);
     if (p->dred) cudaFree(p->dred);
     if (p->load_vec) cudaFree(p->load_vec);
+    if (p->fbuf) cudaFree(p->fbuf);
     if (p->pin) cudaStreamDestroy(p->pin);
     if (p->pout) cudaStreamDestroy(p->pout);
     for (auto& t : p->owned)
@@ -1712,6 +1714,77 @@ int sfem_cuda_ipc_open_handle(const void* handle, void** d_ptr) {
 
 int sfem_cuda_ipc_close(void* d_ptr) {
   return guarded([&] { ck(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle"); });
+}
+
+
+int sfem_cuda_solve_field(sfem_plan p, int field, const double* params, int nparams, int compute_residual,
+                          double* h_u, double* report) {
+  return guarded([&] {
+    require(p && report, "solve_field: null argument");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = p->ctx->stream;
+    const long long last = p->ext[p->dim - 1], pitch = p->pitch;
+    ensure_work(p);
+    const size_t elems = padded_elems(p, pitch);
+    if (!p->fbuf) ck(cudaMalloc(&p->fbuf, elems * sizeof(double)), "cudaMalloc(load)");
+    cudaEvent_t ev[3];
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    struct Ev {
+      cudaEvent_t* e;
+      ~Ev() {
+        for (int i = 0; i < 3; ++i) cudaEventDestroy(e[i]);
+      }
+    } guard{ev};
+    ck(cudaEventRecord(ev[0], s), "event");
+    if (sfem_cuda_fem_load(p, field, params, nparams, p->fbuf, pitch, s) != 0) throw std::runtime_error(g_err);
+    ck(cudaEventRecord(ev[1], s), "event");
+    ck(cudaMemcpyAsync(p->dwork, p->fbuf, elems * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
+    ck(cudaEventRecord(ev[2], s), "event");
+    run_steps(p, p->dwork, pitch, s, false);
+    ck(cudaEventRecord(p->ev[1], s), "event");
+    ck(cudaStreamSynchronize(s), "sync");
+    report[0] = event_seconds(ev[0], ev[1]);  // seconds_load
+    report[1] = event_seconds(ev[2], p->ev[1]);  // seconds_solve
+    report[2] = std::nan("");
+    report[3] = std::nan("");
+    if (compute_residual && sfem_cuda_residual(p, p->dwork, p->fbuf, pitch, &report[2]) != 0)
+      throw std::runtime_error(g_err);
+    if (field != SFEM_FIELD_CONSTANT &&
+        sfem_cuda_max_error(p, field, params, nparams, p->dwork, pitch, &report[3]) != 0)
+      throw std::runtime_error(g_err);
+    if (h_u) {
+      const size_t dense = static_cast<size_t>(p->rows) * last;
+      if (!p->dstage) ck(cudaMalloc(&p->dstage, dense * sizeof(double)), "cudaMalloc(stage)");
+      ck(cudaMemcpy2DAsync(p->dstage, last * sizeof(double), p->dwork, pitch * sizeof(double), last * sizeof(double),
+                           p->rows, cudaMemcpyDeviceToDevice, s),
+         "repitch");
+      ck(cudaMemcpyAsync(h_u, p->dstage, dense * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaStreamSynchronize(s), "sync");
+    }
+  });
+}
+
+int sfem_cuda_apply_operator_host(sfem_plan p, const double* h_v, double* h_y) {
+  return guarded([&] {
+    require(p && h_v && h_y, "apply_operator_host: null argument");
+    ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
+    cudaStream_t s = p->ctx->stream;
+    const long long last = p->ext[p->dim - 1], pitch = p->pitch;
+    ensure_work(p);
+    const size_t elems = padded_elems(p, pitch), dense = static_cast<size_t>(p->rows) * last;
+    if (!p->fbuf) ck(cudaMalloc(&p->fbuf, elems * sizeof(double)), "cudaMalloc(load)");
+    if (!p->dstage) ck(cudaMalloc(&p->dstage, dense * sizeof(double)), "cudaMalloc(stage)");
+    ck(cudaMemcpyAsync(p->dstage, h_v, dense * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    ck(cudaMemcpy2DAsync(p->dwork, pitch * sizeof(double), p->dstage, last * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyDeviceToDevice, s),
+       "repitch");
+    apply_sweeps(p, p->dwork, p->fbuf, nullptr, pitch, s);
+    ck(cudaMemcpy2DAsync(p->dstage, last * sizeof(double), p->fbuf, pitch * sizeof(double), last * sizeof(double),
+                         p->rows, cudaMemcpyDeviceToDevice, s),
+       "repitch");
+    ck(cudaMemcpyAsync(h_y, p->dstage, dense * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+  });
 }
 
 }  // extern "C"

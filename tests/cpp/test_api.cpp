@@ -214,6 +214,46 @@ static void deterministic(TableSet& tables) {
   CHECK(max_diff(u1, u2) == 0.0);
 }
 
+// solve(spec, options) of the reference's manufactured cases, every step on
+// the device: the residual check (poisson.cpp:785-789) and the discretisation
+// error (test_poisson.cpp convergence tests: high order, error shrinks with K)
+static void manufactured_solve() {
+  for (int K : {4, 8}) {
+    ProblemSpec spec;
+    spec.dimension = 2;
+    spec.lengths = {1.0, 1.0};
+    spec.elements = {K, K};
+    spec.orders = {4, 4};
+    spec.shift = 1.0;
+    SolveOptions opt;
+    opt.compute_residual = true;
+    const SolveReport r = solve(spec, Field::manufactured("poisson2d"), opt);
+    CHECK(r.residual_rel.has_value() && *r.residual_rel < 1e-11);
+    CHECK(r.error_uniform.has_value() && *r.error_uniform < (K == 4 ? 5e-2 : 5e-3));
+    CHECK(r.seconds_solve > 0 && r.seconds_load > 0);
+    CHECK(r.solution.classes.size() == 4);
+  }
+  CHECK_THROWS(Field::manufactured("nope"));
+}
+
+// A (A^-1 f) == f through the dense-dof operator
+static void operator_inverts_solve(TableSet& tables) {
+  ProblemSpec spec;
+  spec.dimension = 3;
+  spec.lengths = {1.0, 2.0, 1.0};
+  spec.elements = {5, 4, 6};
+  spec.orders = {3, 2, 4};
+  spec.shift = 0.5;
+  Plan plan(tables.context(), spec);
+  std::vector<double> f(static_cast<size_t>(plan.unknowns())), u(f.size()), y(f.size());
+  std::mt19937 rng(9);
+  std::uniform_real_distribution<double> d(-1.0, 1.0);
+  for (auto& v : f) v = d(rng);
+  plan.solve_dof(f.data(), u.data());
+  plan.apply_operator_dof(u.data(), y.data());
+  CHECK(max_diff(y, f) < 1e-11);
+}
+
 int main() {
   TableSet tables;
   roundtrip_identities(tables);
@@ -221,6 +261,8 @@ int main() {
   solve_vs_dense(tables);
   rejects_invalid(tables);
   deterministic(tables);
+  manufactured_solve();
+  operator_inverts_solve(tables);
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
