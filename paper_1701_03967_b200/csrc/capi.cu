@@ -193,8 +193,16 @@ struct Step {
   bool bulk_rows = false;  // fused last-axis sweep with per-row bulk copies
   TmaGeom geo{};
   cuuint64_t dims[4] = {1, 1, 1, 1}, strides[3] = {0, 0, 0};
+  cuuint32_t box[4] = {0, 0, 0, 0};  // {0,..}: the plain box {8, boxp, 1, 1}
   const double* map_ptr = nullptr;
   alignas(64) CUtensorMap map;
+  // out of place (blocked schedule): load from buffer src_buf, store through
+  // smap into dst_buf (0 = the caller's tensor, 1 = the plan's blocked scratch)
+  int src_buf = 0, dst_buf = 0;
+  cuuint64_t sdims[4] = {1, 1, 1, 1}, sstrides[3] = {0, 0, 0};
+  cuuint32_t sbox[4] = {0, 0, 0, 0};
+  const double* smap_ptr = nullptr;
+  alignas(64) CUtensorMap smap;
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -209,15 +217,27 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-void encode_map(Step& s, const double* data) {
-  if (s.map_ptr == data) return;
-  const cuuint32_t box[4] = {8u, static_cast<cuuint32_t>(s.geo.boxp), 1u, 1u};
+void encode4(CUtensorMap* m, const double* data, const cuuint64_t* dims, const cuuint64_t* strides,
+             const cuuint32_t* box_in, int boxp) {
+  const cuuint32_t plain[4] = {8u, static_cast<cuuint32_t>(boxp), 1u, 1u};
+  const cuuint32_t* box = box_in[0] ? box_in : plain;
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode_fn()(&s.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(data), s.dims,
-                                 s.strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(data), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+void encode_map(Step& s, const double* data) {
+  if (s.map_ptr == data) return;
+  encode4(&s.map, data, s.dims, s.strides, s.box, s.geo.boxp);
   s.map_ptr = data;
+}
+
+void encode_smap(Step& s, const double* data) {
+  if (s.smap_ptr == data) return;
+  encode4(&s.smap, data, s.sdims, s.sstrides, s.sbox, s.geo.boxp);
+  s.smap_ptr = data;
 }
 
 }  // namespace
@@ -356,19 +376,26 @@ Step rows_step(const View& v, int mode) {
 }
 
 // Launch a list of steps on `data` (in place).
-void launch_steps(std::vector<Step>& steps, double* data, sfem_ctx ctx, cudaStream_t stream,
-                  std::vector<cudaEvent_t>* kev) {
+void launch_steps(std::vector<Step>& steps, double* user, sfem_ctx ctx, cudaStream_t stream,
+                  std::vector<cudaEvent_t>* kev, double* scratch = nullptr) {
   for (size_t i = 0; i < steps.size(); ++i) {
     Step& s = steps[i];
+    double* data = s.src_buf ? scratch : user;
+    double* dst = s.dst_buf ? scratch : user;
     s.ls.src = data;
     s.ls.dst = data;
     if (kev) ck(cudaEventRecord((*kev)[i], stream), "event");
     const DevTable& dt = s.table->dev;
     const SymbolInfo* sym = s.mode == kForwardDivideInverse ? &s.sym : nullptr;
     const bool aligned = (reinterpret_cast<unsigned long long>(data) % 16) == 0;
-    if (s.tma && aligned) {
+    if (s.tma && data != dst) {  // blocked schedule: out-of-place TMA sweep
+      require(aligned && reinterpret_cast<unsigned long long>(dst) % 16 == 0, "blocked sweep: unaligned tensor");
       encode_map(s, data);
-      ck(launch_sweep_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
+      encode_smap(s, dst);
+      ck(launch_sweep_tma(dt, &s.map, &s.smap, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
+    } else if (s.tma && aligned) {
+      encode_map(s, data);
+      ck(launch_sweep_tma(dt, &s.map, nullptr, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
     } else if (s.bulk_rows && aligned) {
       RowSegs rs{};
       rs.n = 1;
@@ -406,6 +433,10 @@ struct sfem_plan_s {
   long long pitch = 0;
   long long rows = 0;  // product of leading extents
   std::vector<Step> steps;
+  bool blocked = false;         // 3-D blocked schedule (build_blocked_steps)
+  double* bwork = nullptr;      // its scratch tensor [x_hi][L1][x_lo][bpitch]
+  size_t belems = 0;
+  long long bpitch = 0;
   double* dwork = nullptr;
   double* dstage = nullptr;  // dense host-transfer staging
   // pipelined host solves (sfem_cuda_solve_host_batch): kSlots in-flight
@@ -441,8 +472,117 @@ View plan_view(const sfem_plan_s* p, long long pitch) {
   return v;
 }
 
+// Blocked schedule (3-D, TMA kernels on axes 0 and 1, bulk rows on axis 2):
+// axis 0 is split x = x_hi*xblk + x_lo and stored in the plan's scratch as
+// [x_hi][L1][x_lo][bpitch] (x_lo between y and z), so the axis-0 sweep reads
+// groups of xblk 64-byte rows 8*bpitch bytes apart instead of 575 rows
+// 2.65 MB apart (one DRAM page / TLB reach each; copy-only TMA time 0.98 ms
+// vs 0.47 ms for axis 1, profiles/r1g_*).  Order: axis 1 forward
+// (caller's tensor -> scratch), axis 0 forward (scratch, in place), fused
+// axis 2 (scratch), axis 0 inverse, axis 1 inverse (scratch -> caller's).
+constexpr int kXBlk = 8;
+
+bool blocked_ok(const sfem_plan_s* p, long long pitch) {
+  if (p->dim != 3 || !p->use_fast || std::getenv("SFEM_PLAIN")) return false;
+  const DevTable& t0 = p->tables[0]->dev;
+  const DevTable& t1 = p->tables[1]->dev;
+  const DevTable& t2 = p->tables[2]->dev;
+  const long long nhi = (p->ext[0] + kXBlk - 1) / kXBlk;
+  return has_tma_sweep(t0.n, t0.K) && has_tma_sweep(t1.n, t1.K) && has_bulk_rows(t2.n, t2.K) &&
+         kXBlk * nhi <= 576 && nhi <= 256 && (pitch * 8) % 16 == 0 && ((t2.L + 1) & ~1) <= pitch;
+}
+
+void build_blocked_steps(sfem_plan_s* p, long long pitch) {
+  const long long L0 = p->ext[0], L1 = p->ext[1], L2 = p->ext[2];
+  const long long bp = (L2 + 3) & ~3LL, X = kXBlk, nhi = (L0 + X - 1) / X;
+  p->bpitch = bp;
+  p->belems = static_cast<size_t>(nhi) * X * L1 * bp;
+  const View v = plan_view(p, pitch);
+  // blocked tensor strides (bytes): z 8, x_lo bp*8, y X*bp*8, x_hi L1*X*bp*8
+  const cuuint64_t sxlo = bp * 8, sy = X * bp * 8, sxhi = L1 * X * bp * 8;
+  auto axis1 = [&](int mode) {
+    Step s = strided_step(v, 1, mode);  // plain geometry: d0 z, d1 y (swept), d2 x
+    require(s.tma, "blocked schedule: axis-1 TMA step");
+    // the blocked side: {z, y, x_lo, x_hi}, the tile's x split
+    cuuint64_t* bd = mode == kForward ? s.sdims : s.dims;
+    cuuint64_t* bs = mode == kForward ? s.sstrides : s.strides;
+    const cuuint64_t pd[4] = {s.dims[0], s.dims[1], s.dims[2], s.dims[3]};
+    const cuuint64_t ps[3] = {s.strides[0], s.strides[1], s.strides[2]};
+    if (mode == kForward) {
+      for (int i = 0; i < 4; ++i) s.dims[i] = pd[i];
+      for (int i = 0; i < 3; ++i) s.strides[i] = ps[i];
+    } else {
+      for (int i = 0; i < 4; ++i) s.sdims[i] = pd[i];
+      for (int i = 0; i < 3; ++i) s.sstrides[i] = ps[i];
+    }
+    bd[0] = L2;
+    bd[1] = L1;
+    bd[2] = X;
+    bd[3] = nhi;
+    bs[0] = sy;
+    bs[1] = sxlo;
+    bs[2] = sxhi;
+    s.geo.xblk = X;
+    s.geo.ld_mode = mode == kForward ? kBoxPlain : kBoxSplit;
+    s.geo.st_mode = mode == kForward ? kBoxSplit : kBoxPlain;
+    s.src_buf = mode == kForward ? 0 : 1;
+    s.dst_buf = mode == kForward ? 1 : 0;
+    return s;
+  };
+  auto axis0 = [&](int mode) {
+    Step s = strided_step(v, 0, mode);  // table / line set of axis 0; geometry replaced
+    require(s.tma, "blocked schedule: axis-0 TMA step");
+    s.dims[0] = L2;
+    s.dims[1] = X;
+    s.dims[2] = nhi;
+    s.dims[3] = L1;
+    s.strides[0] = sxlo;
+    s.strides[1] = sxhi;
+    s.strides[2] = sy;
+    s.box[0] = 8;
+    s.box[1] = static_cast<cuuint32_t>(X);
+    s.box[2] = static_cast<cuuint32_t>(nhi);
+    s.box[3] = 1;
+    s.geo.nbox = 1;
+    s.geo.boxp = static_cast<int>(X * nhi);
+    s.geo.nblk0 = (L2 + 7) / 8;
+    s.geo.ext0 = L2;
+    s.geo.ext2 = L1;
+    s.geo.ntiles = s.geo.nblk0 * L1;
+    s.geo.xblk = X;
+    s.geo.ld_mode = s.geo.st_mode = kBoxSwept;
+    s.src_buf = s.dst_buf = 1;
+    return s;
+  };
+  Step rows = rows_step(v, kForwardDivideInverse);
+  require(rows.bulk_rows, "blocked schedule: bulk-row step");
+  rows.ls.nlines = nhi * L1 * X;
+  rows.ls.n1 = rows.ls.nlines;
+  rows.ls.os1 = bp;
+  SymbolInfo& sy_ = rows.sym;
+  sy_.nlead = 3;
+  sy_.lead_ext[0] = nhi;
+  sy_.lead_ext[1] = L1;
+  sy_.lead_ext[2] = X;
+  sy_.xblk = static_cast<int>(X);
+  sy_.x_ext = L0;
+  rows.src_buf = rows.dst_buf = 1;
+  p->steps.clear();
+  p->steps.push_back(axis1(kForward));
+  p->steps.push_back(axis0(kForward));
+  p->steps.push_back(rows);
+  p->steps.push_back(axis0(kInverse));
+  p->steps.push_back(axis1(kInverse));
+  p->blocked = true;
+}
+
 void build_steps(sfem_plan_s* p, long long pitch) {
   const int N = p->dim;
+  p->blocked = false;
+  if (blocked_ok(p, pitch)) {
+    build_blocked_steps(p, pitch);
+    return;
+  }
   const View v = plan_view(p, pitch);
   p->steps.clear();
   for (int a = 0; a < N - 1; ++a) p->steps.push_back(strided_step(v, a, kForward));
@@ -452,7 +592,11 @@ void build_steps(sfem_plan_s* p, long long pitch) {
 
 void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
   if (pitch != p->pitch) build_steps(p, pitch), p->pitch = pitch;
-  launch_steps(p->steps, data, p->ctx, stream, events ? &p->kev : nullptr);
+  if (p->blocked && !p->bwork) {
+    ck(cudaMalloc(&p->bwork, p->belems * sizeof(double)), "cudaMalloc(blocked scratch)");
+    ck(cudaMemsetAsync(p->bwork, 0, p->belems * sizeof(double), stream), "memset(blocked scratch)");
+  }
+  launch_steps(p->steps, data, p->ctx, stream, events ? &p->kev : nullptr, p->bwork);
 }
 
 // Reference ProblemSpec::validate (poisson.cpp:32-47), with per-axis coefficients.
@@ -1008,6 +1152,7 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
     if (!p) return;
     cudaSetDevice(p->ctx->device);
     if (p->dwork) cudaFree(p->dwork);
+    if (p->bwork) cudaFree(p->bwork);
     if (p->dstage) cudaFree(p->dstage);
     for (int b = 0; b < sfem_plan_s::kSlots; ++b) {
       if (p->pwork[b]) cudaFree(p->pwork[b]);

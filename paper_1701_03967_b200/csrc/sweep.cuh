@@ -56,6 +56,11 @@ struct SymbolInfo {
   double lead_f[kMaxDim];
   double shift;
   double f_last;
+  // xblk > 0 (3-D blocked layout): rows are ordered (x_hi, y, x_lo) with
+  // lead_ext {nhi, L1, xblk}; x = x_hi*xblk + x_lo indexes lead_eig[0]
+  // (x >= x_ext: a padding row), y lead_eig[1].
+  int xblk;
+  long long x_ext;
 };
 
 enum SweepMode { kForward = 0, kInverse = 1, kForwardDivideInverse = 2 };
@@ -63,18 +68,30 @@ enum SweepMode { kForward = 0, kInverse = 1, kForwardDivideInverse = 2 };
 // Tile decomposition for the TMA strided kernels: the tensor is viewed as 4-D
 // (d0 = last axis, d1 = swept axis, d2/d3 = remaining axes, size 1 if absent);
 // a tile is 8 consecutive d0 indices x all d1 positions at one (d2, d3).
+//
+// Box coordinates per tensor map (TmaGeom::ld_mode / st_mode), the tile being
+// (c0 = first last-axis index, c2, c3) of the grid:
+//   kBoxPlain    (c0, j*boxp, c2, c3)               box {8, boxp, 1, 1}
+//   kBoxSwept    (c0, 0, 0, c2): the swept axis is stored blocked as
+//                (x_hi, x_lo) with x = x_hi*xblk + x_lo; one box
+//                {8, xblk, nhi, 1} brings all positions (nbox = 1)
+//   kBoxSplit    (c0, j*boxp, c2 % xblk, c2 / xblk): the tile's fixed
+//                coordinate c2 is blocked in this tensor
+enum BoxMode { kBoxPlain = 0, kBoxSwept = 1, kBoxSplit = 2 };
 struct TmaGeom {
   int nbox, boxp;      // boxes along d1 (boxp positions each, nbox*boxp >= L)
   long long nblk0;     // ceil(L_d0 / 8)
   long long ext0;      // L_d0 (extent of the last axis)
   long long ext2;      // extent of d2
   long long ntiles;    // nblk0 * ext2 * ext3
+  int ld_mode, st_mode, xblk;
 };
 
-// Strided sweep through TMA (sweep_fast.cu).  `tmap` is a CUtensorMap (64-byte
-// aligned opaque blob) describing the in-place tensor.
-cudaError_t launch_sweep_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
-                             cudaStream_t stream);
+// Strided sweep through TMA (sweep_fast.cu).  `tmap` / `smap` are CUtensorMaps
+// (64-byte aligned opaque blobs) of the tensor the tile is loaded from and
+// stored to (the same map for an in-place sweep).
+cudaError_t launch_sweep_tma(const DevTable& t, const void* tmap, const void* smap, const TmaGeom& geo, int mode,
+                             int analysis, cudaStream_t stream);
 bool has_tma_sweep(int n, int K);
 // Fused last-axis sweep with per-row bulk copies (K = 64 specialisations).
 // A row is the concatenation of `n` segments: segment s of row q holds
