@@ -82,6 +82,14 @@ int sfem_cuda_plan_shape(sfem_plan plan, long long* extents, long long* pitch, l
 /* Kernel launches per solve (2N-1 for the fused schedule). */
 int sfem_cuda_plan_launches(sfem_plan plan, int* launches);
 
+/* Algorithm of the plan's solves (reference SolveOptions::algorithm,
+ * poisson.hpp:64-70): 0 = FullDiagonalization (default), 1 =
+ * PartialDiagonalization (poisson.cpp:671-745: expansions along axes 1..N-1,
+ * a banded SPD solve along axis 0 per frequency line; dimension >= 2).  An
+ * indefinite line raises the reference's error in the synchronous host
+ * entry points. */
+int sfem_cuda_plan_set_algorithm(sfem_plan plan, int algorithm);
+
 /* Device-resident solve, in place: d_data holds the load (dof layout, last
  * axis padded to `pitch` elements) and receives u.  Replaces
  * solve_with_load's timed core run_full_diagonalization (poisson.cpp:637-669,

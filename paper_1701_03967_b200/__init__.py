@@ -91,6 +91,7 @@ _SIGS = [
     ("sfem_cuda_apply_operator", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _vp]),
     ("sfem_cuda_residual", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_longlong, _dp]),
     ("sfem_cuda_max_error", ctypes.c_int, [_vp, ctypes.c_int, _dp, ctypes.c_int, _vp, ctypes.c_longlong, _dp]),
+    ("sfem_cuda_plan_set_algorithm", ctypes.c_int, [_vp, ctypes.c_int]),
     ("sfem_cuda_solve_field", ctypes.c_int, [_vp, ctypes.c_int, _dp, ctypes.c_int, ctypes.c_int, _dp, _dp]),
     ("sfem_cuda_apply_operator_host", ctypes.c_int, [_vp, _dp, _dp]),
     ("sfem_cuda_peer_create", ctypes.c_int,
@@ -356,7 +357,7 @@ class ProblemSpec:
 
 @dataclass
 class SolveOptions:
-    """SolveOptions (poisson.hpp:64-70); only FullDiagonalization runs on the GPU path."""
+    """SolveOptions (poisson.hpp:64-70); algorithm "full" (a) or "partial" (b)."""
     algorithm: str = "full"
     threads: int = 0
     compute_residual: bool = False
@@ -418,6 +419,13 @@ class Plan:
         nl = ctypes.c_int()
         _check(lib.sfem_cuda_plan_launches(h, ctypes.byref(nl)))
         self.launches = nl.value
+
+    def set_algorithm(self, algorithm: str):
+        """'full' (algorithm (a), default) or 'partial' (algorithm (b), poisson.cpp:671-745)."""
+        if algorithm not in ("full", "partial"):
+            raise Error(f"solve: unknown algorithm '{algorithm}'")
+        _check(lib.sfem_cuda_plan_set_algorithm(self.handle, 0 if algorithm == "full" else 1))
+        self.algorithm = algorithm
 
     @property
     def padded_shape(self):
@@ -531,10 +539,9 @@ def solve_with_load(spec: ProblemSpec, load, tables: Optional[TableSet] = None,
     tensor; the solution comes back in the same form.  `tables` is accepted for
     interface parity (device tables are owned by the plan)."""
     options = options or SolveOptions()
-    if options.algorithm != "full":
-        raise Error("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path")
     ctx = tables.ctx if tables is not None else None
     plan = Plan(spec, ctx)
+    plan.set_algorithm(options.algorithm)
     if isinstance(load, GridFunctionND):
         sol, sec = plan.solve_classes(load)
     else:
@@ -577,6 +584,6 @@ def solve(spec: ProblemSpec, rhs: Field, options: Optional[SolveOptions] = None,
     the residual check and, for fields with a known solution, error_uniform.
     The solution comes back as a dense dof tensor."""
     options = options or SolveOptions()
-    if options.algorithm != "full":
-        raise Error("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path")
-    return Plan(spec, ctx).solve_field(rhs, options.compute_residual)
+    plan = Plan(spec, ctx)
+    plan.set_algorithm(options.algorithm)
+    return plan.solve_field(rhs, options.compute_residual)

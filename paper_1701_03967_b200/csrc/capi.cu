@@ -28,6 +28,7 @@
 
 #include "../../include/sfem_cuda.h"
 #include "dist.cuh"
+#include "banded.cuh"
 #include "fem_ops.cuh"
 #include "sweep.cuh"
 #include "table.hpp"
@@ -433,6 +434,12 @@ struct sfem_plan_s {
   long long pitch = 0;
   long long rows = 0;  // product of leading extents
   std::vector<Step> steps;
+  int algorithm = 0;            // 0: full diagonalisation (a), 1: partial (b)
+  std::vector<Step> pfwd, pinv; // algorithm (b): forward / inverse sweeps of axes N-1 .. 1
+  BandArgs band{};              // algorithm (b): the axis-0 line solves
+  double* cbuf = nullptr;       // their Thomas coefficients
+  unsigned long long* dfail = nullptr;
+  unsigned long long* hfail = nullptr;  // pinned copy of the failure flag
   bool blocked = false;         // 3-D blocked schedule (build_blocked_steps)
   double* bwork = nullptr;      // its scratch tensor [x_hi][L1][x_lo][bpitch]
   size_t belems = 0;
@@ -590,7 +597,108 @@ void build_steps(sfem_plan_s* p, long long pitch) {
   for (int a = N - 2; a >= 0; --a) p->steps.push_back(strided_step(v, a, kInverse));
 }
 
+// Algorithm (b) (poisson.cpp:671-745): forward expansions along axes N-1..1
+// (the last axis as rows), the axis-0 line solves (banded.cu), inverse
+// expansions along axes 1..N-1.
+void build_partial_steps(sfem_plan_s* p, long long pitch) {
+  const int N = p->dim;
+  const View v = plan_view(p, pitch);
+  p->pfwd.clear();
+  p->pinv.clear();
+  p->pfwd.push_back(rows_step(v, kForward));
+  for (int a = N - 2; a >= 1; --a) p->pfwd.push_back(strided_step(v, a, kForward));
+  for (int a = 1; a <= N - 2; ++a) p->pinv.push_back(strided_step(v, a, kInverse));
+  p->pinv.push_back(rows_step(v, kInverse));
+  BandArgs& b = p->band;
+  b = BandArgs{};
+  const HostTable& h = p->tables[0]->host;
+  const int n = p->orders[0], np = n + 1, m = n - 1;
+  b.n = n;
+  b.K = p->elements[0];
+  b.L = p->ext[0];
+  std::vector<long long> st(N);
+  st[N - 1] = 1;
+  if (N >= 2) st[N - 2] = pitch;
+  for (int i = N - 3; i >= 0; --i) st[i] = st[i + 1] * p->ext[i + 1];
+  b.inner = st[0];
+  b.outer = 1;
+  b.pitch = pitch;
+  b.last = p->ext[N - 1];
+  b.f0 = p->factors[0];
+  b.shift = p->shift;
+  b.nfreq = N - 1;
+  for (int i = 1; i < N; ++i) {
+    b.fext[i - 1] = p->ext[i];
+    b.eig[i - 1] = p->tables[i]->dev.eig;
+    b.f[i - 1] = p->factors[i];
+  }
+  auto A = [&](int r, int c) { return h.stiffness[static_cast<size_t>(r) * np + c]; };
+  auto C = [&](int r, int c) { return h.mass[static_cast<size_t>(r) * np + c]; };
+  b.A00 = A(0, 0);
+  b.A0n = A(0, n);
+  b.C00 = C(0, 0);
+  b.C0n = C(0, n);
+  for (int l = 0; l < m; ++l) {
+    b.lam[l] = h.interior_values[l];
+    double pa0 = 0, pan = 0, pc0 = 0, pcn = 0;
+    for (int c = 0; c < m; ++c) {
+      const double vcl = h.interior_vectors[static_cast<size_t>(c) * m + l];
+      b.V[c][l] = vcl;
+      pa0 += vcl * A(1 + c, 0);
+      pan += vcl * A(1 + c, n);
+      pc0 += vcl * C(1 + c, 0);
+      pcn += vcl * C(1 + c, n);
+    }
+    b.PA0[l] = pa0;
+    b.PAn[l] = pan;
+    b.PC0[l] = pc0;
+    b.PCn[l] = pcn;
+  }
+}
+
+void run_partial(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream) {
+  if (pitch != p->band.pitch || p->pfwd.empty()) build_partial_steps(p, pitch);
+  const size_t lines = static_cast<size_t>(p->band.inner * p->band.outer);
+  if (!p->cbuf) {
+    ck(cudaMalloc(&p->cbuf, static_cast<size_t>(p->band.K) * lines * sizeof(double)), "cudaMalloc(band scratch)");
+    ck(cudaMalloc(&p->dfail, sizeof(unsigned long long)), "cudaMalloc(flag)");
+    ck(cudaMallocHost(&p->hfail, sizeof(unsigned long long)), "cudaMallocHost(flag)");
+  }
+  ck(cudaMemsetAsync(p->dfail, 0xff, sizeof(unsigned long long), stream), "memset(flag)");
+  launch_steps(p->pfwd, data, p->ctx, stream, nullptr);
+  ck(launch_band_lines(data, p->cbuf, p->band, p->dfail, stream), "band line solves");
+  ck(cudaMemcpyAsync(p->hfail, p->dfail, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream), "flag");
+  launch_steps(p->pinv, data, p->ctx, stream, nullptr);
+}
+
+// After a synchronised algorithm-(b) solve: the reference's error for an
+// indefinite line (poisson.cpp:720-725), with its line index r (row-major
+// over the frequency extents of axes 1..N-1).
+void check_partial(const sfem_plan_s* p) {
+  if (p->algorithm != 1 || !p->hfail || *p->hfail == ~0ULL) return;
+  long long rem = static_cast<long long>(*p->hfail), r = 0, mul = 1;
+  double sigma = p->shift;
+  const int N = p->dim;
+  std::vector<long long> t(N, 0);
+  for (int ax = N - 1; ax >= 1; --ax) {
+    const long long ext = ax == N - 1 ? p->band.pitch : p->ext[ax];
+    t[ax] = rem % ext;
+    rem /= ext;
+  }
+  for (int ax = N - 1; ax >= 1; --ax) {
+    r += t[ax] * mul;
+    mul *= p->ext[ax];
+    sigma += p->factors[ax] * p->tables[ax]->host.eig_coeff[t[ax]];
+  }
+  fail("solve: indefinite 1D system at transformed frequency " + std::to_string(r) + " (sigma " +
+       std::to_string(sigma) + "); shift too negative");
+}
+
 void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
+  if (p->algorithm == 1) {
+    run_partial(p, data, pitch, stream);
+    return;
+  }
   if (pitch != p->pitch) build_steps(p, pitch), p->pitch = pitch;
   if (p->blocked && !p->bwork) {
     ck(cudaMalloc(&p->bwork, p->belems * sizeof(double)), "cudaMalloc(blocked scratch)");
@@ -1153,6 +1261,9 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
     cudaSetDevice(p->ctx->device);
     if (p->dwork) cudaFree(p->dwork);
     if (p->bwork) cudaFree(p->bwork);
+    if (p->cbuf) cudaFree(p->cbuf);
+    if (p->dfail) cudaFree(p->dfail);
+    if (p->hfail) cudaFreeHost(p->hfail);
     if (p->dstage) cudaFree(p->dstage);
     for (int b = 0; b < sfem_plan_s::kSlots; ++b) {
       if (p->pwork[b]) cudaFree(p->pwork[b]);
@@ -1234,6 +1345,7 @@ int sfem_cuda_solve_host(sfem_plan p, const double* h_load, double* h_u, double*
        "repitch");
     ck(cudaMemcpyAsync(h_u, stage, dense * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
+    check_partial(p);
     if (seconds) *seconds = event_seconds(p->ev[0], p->ev[1]);
   });
 }
@@ -1311,6 +1423,16 @@ int sfem_cuda_solve_device_timed(sfem_plan p, double* d_data, long long pitch, i
     require(p && d_data && reps >= 1, "solve_device_timed: bad argument");
     ck(cudaSetDevice(p->ctx->device), "cudaSetDevice");
     cudaStream_t s = p->ctx->stream;
+    if (p->algorithm == 1) {  // algorithm (b): whole-solve time only
+      ck(cudaEventRecord(p->ev[0], s), "event");
+      for (int r = 0; r < reps; ++r) run_steps(p, d_data, pitch, s, false);
+      ck(cudaEventRecord(p->ev[1], s), "event");
+      ck(cudaStreamSynchronize(s), "sync");
+      if (total_ms) *total_ms = event_seconds(p->ev[0], p->ev[1]) * 1e3 / reps;
+      if (kernel_ms)
+        for (size_t i = 0; i < p->steps.size(); ++i) kernel_ms[i] = 0.0;
+      return;
+    }
     std::vector<double> acc(p->steps.size(), 0.0);
     double total = 0;
     for (int r = 0; r < reps; ++r) {
@@ -1929,6 +2051,17 @@ int sfem_cuda_apply_operator_host(sfem_plan p, const double* h_v, double* h_y) {
        "repitch");
     ck(cudaMemcpyAsync(h_y, p->dstage, dense * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+
+int sfem_cuda_plan_set_algorithm(sfem_plan p, int algorithm) {
+  return guarded([&] {
+    require(p != nullptr, "plan_set_algorithm: null plan");
+    require(algorithm == 0 || algorithm == 1, "plan_set_algorithm: algorithm must be 0 (full) or 1 (partial)");
+    if (algorithm == 1) require(p->dim >= 2, "solve: partial diagonalization needs dimension >= 2");
+    p->algorithm = algorithm;
+    p->pfwd.clear();
   });
 }
 
