@@ -533,7 +533,10 @@ def main():
             "config": {"workload": desc, "unknowns_per_gpu": U, "extents": ext, "device_pitch": plan.pitch,
                        "l2_flush": "none needed: 1.52 GB tensor > 126 MB L2", "parallelism": f"replicas x{world}",
                        "dist_error": getattr(args, "dist_error", None),
-                       "schedule": "2N-1 sweeps: fwd axes 0..N-2, fused fwd+divide+inv last axis, inv axes N-2..0"},
+                       "schedule": ("2N-1 sweeps; 3-D: fwd axis 1 (caller's tensor -> blocked scratch [x/8][y][x%8][z]), "
+                                    "fwd axis 0, fused fwd+divide+inv axis 2, inv axis 0, inv axis 1 (-> caller's tensor)"
+                                    if len(orders) == 3 else
+                                    "2N-1 sweeps: fwd axes 0..N-2, fused fwd+divide+inv last axis, inv axes N-2..0")},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -353,6 +353,11 @@ class Plan {
   Plan(const Plan&) = delete;
   Plan& operator=(const Plan&) = delete;
   sfem_plan handle() const { return h_; }
+  // SolveOptions::algorithm (poisson.hpp:64-70): FullDiagonalization (a) or
+  // PartialDiagonalization (b, poisson.cpp:671-745; dimension >= 2)
+  void set_algorithm(Algorithm a) {
+    check(sfem_cuda_plan_set_algorithm(h_, a == Algorithm::FullDiagonalization ? 0 : 1));
+  }
   // dense dof-layout load -> u (host buffers); returns device-timed seconds
   double solve_dof(const double* load, double* u) {
     double sec = 0;
@@ -401,10 +406,9 @@ class Plan {
 inline SolveReport solve_with_load(const ProblemSpec& spec, const GridFunctionND& load, TableSet& tables,
                                    const SolveOptions& options = {}) {
   spec.validate();
-  if (options.algorithm != Algorithm::FullDiagonalization)
-    fail("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path");
   require(load.dim() == spec.dimension, "solve: load dimension does not match the problem");
   Plan plan(tables.context(), spec);
+  plan.set_algorithm(options.algorithm);
   SolveReport r;
   r.solution = plan.solve_classes(load, &r.seconds_solve);
   return r;
@@ -414,11 +418,10 @@ inline SolveReport solve_with_load(const ProblemSpec& spec, const GridFunctionND
 // and on request the residual check / uniform error, all on the GPU.
 inline SolveReport solve(const ProblemSpec& spec, const Field& rhs, const SolveOptions& options = {}) {
   spec.validate();
-  if (options.algorithm != Algorithm::FullDiagonalization)
-    fail("solve: only FullDiagonalization (algorithm (a)) runs on the B200 path");
   static TableSet local;
   TableSet& tables = options.tables ? *options.tables : local;
   Plan plan(tables.context(), spec);
+  plan.set_algorithm(options.algorithm);
   return plan.solve_field(rhs, options.compute_residual);
 }
 

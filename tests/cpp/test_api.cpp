@@ -254,6 +254,38 @@ static void operator_inverts_solve(TableSet& tables) {
   CHECK(max_diff(y, f) < 1e-11);
 }
 
+// algorithm (b) agrees with algorithm (a) (both solve the same system)
+static void partial_matches_full(TableSet& tables) {
+  ProblemSpec spec;
+  spec.dimension = 3;
+  spec.lengths = {1.0, 1.0, 1.0};
+  spec.elements = {6, 5, 4};
+  spec.orders = {9, 3, 2};
+  spec.shift = 0.0;
+  GridFunctionND load = GridFunctionND::zeros(spec.axis_specs());
+  std::mt19937 rng(11);
+  std::uniform_real_distribution<double> d(-1.0, 1.0);
+  for (auto& c : load.classes)
+    for (auto& v : c) v = d(rng);
+  load = classes_from_dof(spec.axis_specs(), [&] {
+    // round trip through the dof layout zeroes the boundary slots
+    std::vector<double> dof(static_cast<size_t>(53 * 14 * 7));
+    for (auto& v : dof) v = d(rng);
+    return dof;
+  }());
+  SolveOptions a, b;
+  b.algorithm = Algorithm::PartialDiagonalization;
+  const SolveReport ra = solve_with_load(spec, load, tables, a);
+  const SolveReport rb = solve_with_load(spec, load, tables, b);
+  double w = 0, nrm = 0;
+  for (size_t c = 0; c < ra.solution.classes.size(); ++c)
+    for (size_t i = 0; i < ra.solution.classes[c].size(); ++i) {
+      w = std::max(w, std::abs(ra.solution.classes[c][i] - rb.solution.classes[c][i]));
+      nrm = std::max(nrm, std::abs(ra.solution.classes[c][i]));
+    }
+  CHECK(w <= 1e-12 * nrm);
+}
+
 int main() {
   TableSet tables;
   roundtrip_identities(tables);
@@ -263,6 +295,7 @@ int main() {
   deterministic(tables);
   manufactured_solve();
   operator_inverts_solve(tables);
+  partial_matches_full(tables);
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
