@@ -211,7 +211,7 @@ def run_peer(args, world, rank, local, dist):
     ext = torch.cuda.ExternalStream(ctx.stream)
     xv = plan.x_view()
     L1, L2 = plan.extents[1], plan.extents[2]
-    f_local = np.random.default_rng(1000 + rank).uniform(-1.0, 1.0, (L1, plan.lx, L2))
+    f_local = np.random.default_rng(1000 + rank).uniform(-1.0, 1.0, (plan.lx, L1, L2))
     xv[:, :, :L2].copy_(torch.from_numpy(f_local))
     torch.cuda.synchronize()
     barrier(dist, world)

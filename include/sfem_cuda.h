@@ -193,7 +193,7 @@ int sfem_cuda_dist_phase(sfem_dist dist, int phase, double* d_x, double* d_y, do
  * TMA-stores each finished tile straight into the owning rank's y-slab (peer
  * memory), and the fused axis-0 sweep (forward + divide + inverse) stores its
  * tiles straight back into the source ranks' x-slabs.  Rank r's buffers are
- * plan-owned: x-slab [L1][lx][pitch] (axis-0 rows x0.., laid out y, x, z) and
+ * plan-owned: x-slab [lx][L1][pitch] (axis-0 rows x0.., laid out x, y, z) and
  * y-slab [ly][L0][pitch] (axis-1 rows y0..).  One solve:
  *   PEER_FORWARD, PEER_BARRIER, PEER_AXIS0, PEER_BARRIER, PEER_INVERSE.
  * Replaces run_full_diagonalization (poisson.cpp:637-669), sharded. */

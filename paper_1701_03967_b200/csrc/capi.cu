@@ -1045,7 +1045,7 @@ double red_to_double(unsigned long long b) {
 
 // NVLink slab decomposition with the exchanges fused into the sweeps (3-D,
 // K = 64 tables on axes 0 and 1).  Rank r owns the x-slab [L1][lx_r][pitch]
-// (axis-0 rows x0_r.., laid out y, x, z) and the y-slab [ly_r][L0][pitch]
+// (axis-0 rows x0_r.., laid out x, y, z) and the y-slab [ly_r][L0][pitch]
 // (axis-1 rows y0_r.., laid out y, x, z).
 struct sfem_peer_s {
   sfem_ctx ctx = nullptr;
@@ -1836,12 +1836,12 @@ int sfem_cuda_peer_create(sfem_ctx ctx, int dim, const int* orders, const int* e
       v.use_fast = true;
       return v;
     };
-    d->xv = view(L1, d->lx[rank], 1, 0);  // [y][x][z]
+    d->xv = view(d->lx[rank], L1, 0, 1);  // [x][y][z]
     d->yv = view(d->ly[rank], L0, 1, 0);  // [y][x][z]
     d->fwd_rows.push_back(rows_step(d->xv, kForward));
-    d->fwd_y = strided_step(d->xv, 0, kForward);
+    d->fwd_y = strided_step(d->xv, 1, kForward);
     d->axis0 = strided_step(d->yv, 1, kForward);
-    d->inv_local.push_back(strided_step(d->xv, 0, kInverse));
+    d->inv_local.push_back(strided_step(d->xv, 1, kInverse));
     d->inv_local.push_back(rows_step(d->xv, kInverse));
     require(d->fwd_y.tma && d->axis0.tma, "peer_create: TMA kernels unavailable");
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -1912,7 +1912,7 @@ int sfem_cuda_peer_bind(sfem_peer d, void* const* x_slabs, void* const* y_slabs,
       a.r0[p] = static_cast<int>(d->x0[p]);
       a.n[p] = static_cast<int>(d->lx[p]);
       box_split(d->lx[p], a.nbox[p], a.b[p]);
-      encode_map3(&a.map[p], x_slabs[p], L2, d->lx[p], L1, pitch * 8, d->lx[p] * pitch * 8, a.b[p]);
+      encode_map3(&a.map[p], x_slabs[p], L2, d->lx[p], L1, L1 * pitch * 8, pitch * 8, a.b[p]);
     }
     d->device_barrier = flags != nullptr;
     if (flags)

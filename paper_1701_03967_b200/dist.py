@@ -215,7 +215,7 @@ PEER_FORWARD, PEER_AXIS0, PEER_INVERSE, PEER_BARRIER = 0, 1, 2, 3
 
 class PeerPlan:
     """One rank's share of the fused NVLink solve (3-D, K = 64 on axes 0, 1).
-    Buffers are plan-owned: x-slab [L1][lx][pitch] (laid out y, x, z), y-slab
+    Buffers are plan-owned: x-slab [lx][L1][pitch] (laid out x, y, z), y-slab
     [ly][L0][pitch]."""
 
     def __init__(self, spec: ProblemSpec, nranks: int, rank: int, ctx: Optional[Context] = None):
@@ -257,20 +257,19 @@ class PeerPlan:
 
     # ---- slab data (dense global dof tensor <-> this rank's x-slab) ----
     def x_view(self):
-        """torch view of the plan-owned x-slab [L1][lx][pitch]."""
-        return _wrap_device(self.x_ptr, (self.extents[1], self.lx, self.pitch), self.ctx.device)
+        """torch view of the plan-owned x-slab [lx][L1][pitch]."""
+        return _wrap_device(self.x_ptr, (self.lx, self.extents[1], self.pitch), self.ctx.device)
 
     def scatter_x(self, load: np.ndarray):
         import torch
         v = self.x_view()
-        blk = np.ascontiguousarray(np.transpose(load[self.x0:self.x0 + self.lx], (1, 0, 2)))
+        blk = np.ascontiguousarray(load[self.x0:self.x0 + self.lx])
         v[:, :, :self.extents[2]].copy_(torch.from_numpy(blk))
 
     def gather_x(self) -> np.ndarray:
         import torch
         torch.cuda.synchronize(self.ctx.device)
-        blk = self.x_view()[:, :, :self.extents[2]].cpu().numpy()
-        return np.ascontiguousarray(np.transpose(blk, (1, 0, 2)))
+        return self.x_view()[:, :, :self.extents[2]].cpu().numpy()
 
     def close(self):
         for ptr in self._opened:
