@@ -188,11 +188,17 @@ static void rejects_invalid(TableSet& tables) {
   bad.shift = 1.0;
   bad.elements = {4};
   CHECK_THROWS(bad.validate());
-  ProblemSpec one = spec;
+  // algorithm (b) needs dimension >= 2 (poisson.cpp:674)
+  ProblemSpec one;
+  one.dimension = 1;
+  one.lengths = {1.0};
+  one.elements = {4};
+  one.orders = {2};
   one.shift = 1.0;
+  GridFunctionND load1 = GridFunctionND::zeros(one.axis_specs());
   SolveOptions opt;
   opt.algorithm = Algorithm::PartialDiagonalization;
-  CHECK_THROWS(solve_with_load(one, load, tables, opt));
+  CHECK_THROWS(solve_with_load(one, load1, tables, opt));
 }
 
 // test_poisson.cpp:355-362 (bitwise reproducibility)
