@@ -124,10 +124,18 @@ struct CoefficientArray1D {
 // ---------------------------------------------------------------------------
 // Spectral table (device) and TableSet (poisson.hpp:48-62)
 // ---------------------------------------------------------------------------
+enum class TableFormat { Text = SFEM_TABLE_TEXT, Binary = SFEM_TABLE_BINARY };
+
 class SpectralTable {
  public:
   SpectralTable(Context& ctx, int order, int elements) : order(order), elements(elements) {
     check(sfem_cuda_table_create(ctx.handle(), order, elements, &h_));
+  }
+  // load_table (spectral.hpp:326): the reference's SFEM1 text files or our SFEMB1 binary ones.
+  static std::unique_ptr<SpectralTable> load(Context& ctx, const std::string& path, int order, int elements) {
+    sfem_table h = nullptr;
+    check(sfem_cuda_table_load(ctx.handle(), path.c_str(), order, elements, &h));
+    return std::unique_ptr<SpectralTable>(new SpectralTable(h, order, elements));
   }
   ~SpectralTable() { sfem_cuda_table_destroy(h_); }
   SpectralTable(const SpectralTable&) = delete;
@@ -139,15 +147,35 @@ class SpectralTable {
     check(sfem_cuda_table_export(h_, nullptr, nullptr, nullptr, nullptr, nullptr, e.data()));
     return e;
   }
+  // save_table (spectral.hpp:325); Text writes the reference's file byte for byte.
+  void save(const std::string& path, TableFormat format = TableFormat::Text) const {
+    check(sfem_cuda_table_save(h_, path.c_str(), static_cast<int>(format)));
+  }
   const int order, elements;
 
  private:
+  SpectralTable(sfem_table h, int order, int elements) : order(order), elements(elements), h_(h) {}
   sfem_table h_ = nullptr;
 };
 
+// build_and_save_table (spectral.hpp:320-321), host only.
+inline void build_and_save_table(int order, int elements, const std::string& path,
+                                 TableFormat format = TableFormat::Text) {
+  check(sfem_cuda_table_file_build(order, elements, path.c_str(), static_cast<int>(format)));
+}
+
+// TableSet(cache_dir, write_cache) as the reference's constructor (poisson.hpp:50-52): the
+// cache directory is set on the context, so the plans built on it use it too.
 class TableSet {
  public:
-  explicit TableSet(Context& ctx = default_context()) : ctx_(ctx) {}
+  explicit TableSet(Context& ctx = default_context(), const std::string& cache_dir = {}, bool write_cache = false,
+                    TableFormat format = TableFormat::Binary)
+      : ctx_(ctx) {
+    if (!cache_dir.empty())
+      check(sfem_cuda_ctx_set_table_cache(ctx.handle(), cache_dir.c_str(),
+                                          (write_cache ? SFEM_TABLE_CACHE_WRITE : 0) |
+                                              (format == TableFormat::Binary ? SFEM_TABLE_CACHE_BINARY : 0)));
+  }
   const SpectralTable& get(int order, int elements) {
     auto key = std::make_pair(order, elements);
     auto it = tables_.find(key);

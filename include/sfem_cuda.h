@@ -54,6 +54,37 @@ int sfem_cuda_table_destroy(sfem_table table);
 int sfem_cuda_table_export(sfem_table table, double* values, double* norm_sq, double* p,
                            double* interior_values, double* interior_vectors, double* eig_coeff);
 
+/* Table files and the table cache (reference save_table / load_table /
+ * build_and_save_table, spectral.hpp:316-330 / spectral.cpp:81-236, and
+ * TableSet's cache directory, poisson.hpp:48-62 / poisson.cpp:49-73).
+ *   SFEM_TABLE_TEXT    the reference's "SFEM1" text format (17 significant
+ *                      digits), written byte for byte as save_table writes it
+ *                      and read as load_table reads it (a cache directory the
+ *                      reference filled is used as is);
+ *   SFEM_TABLE_BINARY  "SFEMB1": the same primaries as raw doubles plus an
+ *                      FNV-1a checksum (bit-exact, no text parse).
+ * Loading sniffs the format, checks the header against (order, elements)
+ * with load_table's messages, and rebuilds the derived data as the reference
+ * does (spectral.cpp:209-235).  Writes go to a temporary name and are renamed
+ * into place.
+ *
+ * sfem_cuda_ctx_set_table_cache: every later table of this context (table_create
+ * and the plans' tables) is looked up as sfem_table_n<n>_K<K>.bin, then .txt
+ * (the reference's name), under `dir`; an absent or stale entry is rebuilt and,
+ * with SFEM_TABLE_CACHE_WRITE, written in the format SFEM_TABLE_CACHE_BINARY
+ * selects (else text).  dir NULL or "" turns the cache off (the default).
+ * sfem_cuda_table_file_build / _read work on the host only (no device) --
+ * build_and_save_table, and load_table followed by the export of
+ * sfem_cuda_table_export. */
+enum { SFEM_TABLE_TEXT = 0, SFEM_TABLE_BINARY = 1 };
+enum { SFEM_TABLE_CACHE_WRITE = 1, SFEM_TABLE_CACHE_BINARY = 2 };
+int sfem_cuda_ctx_set_table_cache(sfem_ctx ctx, const char* dir, int flags);
+int sfem_cuda_table_load(sfem_ctx ctx, const char* path, int order, int elements, sfem_table* out);
+int sfem_cuda_table_save(sfem_table table, const char* path, int format);
+int sfem_cuda_table_file_build(int order, int elements, const char* path, int format);
+int sfem_cuda_table_file_read(const char* path, int order, int elements, double* values, double* norm_sq,
+                              double* p, double* interior_values, double* interior_vectors, double* eig_coeff);
+
 /* 1D line operations (reference eigenbasis.hpp:50-79):
  *   SFEM_OP_DECOMPOSE_WEIGHTED  lines::decompose_weighted  (FC_n, eigenbasis.cpp:63-101)
  *   SFEM_OP_DECOMPOSE           lines::decompose           (F_n,  eigenbasis.cpp:103-142)

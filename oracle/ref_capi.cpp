@@ -133,6 +133,28 @@ ProblemSpec make_spec(int dim, const int* orders, const int* elements, const dou
   return spec;
 }
 
+void export_table(const SpectralTable1D& t, double* theta, double* half_cos, double* half_sin, double* values,
+                  double* norm_sq, double* nodal_weight, double* p, double* q, double* interior_values,
+                  double* interior_vectors, double* eig_coeff) {
+  const int m = t.order - 1;
+  auto cp = [](const std::vector<double>& v, double* dst) {
+    if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+  };
+  cp(t.theta, theta);
+  cp(t.half_cos, half_cos);
+  cp(t.half_sin, half_sin);
+  cp(t.values, values);
+  cp(t.norm_sq, norm_sq);
+  cp(t.nodal_weight, nodal_weight);
+  cp(t.p, p);
+  cp(t.q, q);
+  if (m > 0) {
+    cp(t.interior.values, interior_values);
+    cp(t.interior.vectors.a, interior_vectors);
+  }
+  cp(t.eigenvalues_coeff_order(), eig_coeff);
+}
+
 TableSet& tables() {
   static TableSet t;
   return t;
@@ -174,24 +196,35 @@ int sfemref_table(int n, int K, double* theta, double* half_cos, double* half_si
                   double* norm_sq, double* nodal_weight, double* p, double* q, double* interior_values,
                   double* interior_vectors, double* eig_coeff) {
   return guarded([&] {
-    const SpectralTable1D& t = tables().get(n, K);
-    const int m = n - 1;
-    auto cp = [](const std::vector<double>& v, double* dst) {
-      if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(double));
-    };
-    cp(t.theta, theta);
-    cp(t.half_cos, half_cos);
-    cp(t.half_sin, half_sin);
-    cp(t.values, values);
-    cp(t.norm_sq, norm_sq);
-    cp(t.nodal_weight, nodal_weight);
-    cp(t.p, p);
-    cp(t.q, q);
-    if (m > 0) {
-      cp(t.interior.values, interior_values);
-      cp(t.interior.vectors.a, interior_vectors);
-    }
-    cp(t.eigenvalues_coeff_order(), eig_coeff);
+    export_table(tables().get(n, K), theta, half_cos, half_sin, values, norm_sq, nodal_weight, p, q,
+                 interior_values, interior_vectors, eig_coeff);
+  });
+}
+
+// Table files (spectral.cpp:81-236): save_table of the (memoised) table.
+int sfemref_save_table(int n, int K, const char* path) {
+  return guarded([&] { save_table(tables().get(n, K), path); });
+}
+
+// load_table, then the export of sfemref_table.
+int sfemref_load_table(const char* path, int n, int K, double* theta, double* half_cos, double* half_sin,
+                       double* values, double* norm_sq, double* nodal_weight, double* p, double* q,
+                       double* interior_values, double* interior_vectors, double* eig_coeff) {
+  return guarded([&] {
+    const SpectralTable1D t = load_table(path, n, K);
+    export_table(t, theta, half_cos, half_sin, values, norm_sq, nodal_weight, p, q, interior_values,
+                 interior_vectors, eig_coeff);
+  });
+}
+
+// A fresh TableSet over a cache directory (poisson.cpp:49-73), then the export.
+int sfemref_tableset_get(const char* dir, int write_cache, int n, int K, double* theta, double* half_cos,
+                         double* half_sin, double* values, double* norm_sq, double* nodal_weight, double* p,
+                         double* q, double* interior_values, double* interior_vectors, double* eig_coeff) {
+  return guarded([&] {
+    TableSet ts(Precision::Double, dir, write_cache != 0);
+    export_table(ts.get(n, K), theta, half_cos, half_sin, values, norm_sq, nodal_weight, p, q, interior_values,
+                 interior_vectors, eig_coeff);
   });
 }
 

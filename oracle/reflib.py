@@ -32,6 +32,9 @@ def lib():
         L.sfemref_trig_invocations.restype = ctypes.c_ulonglong
         L.sfemref_trig.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp]
         L.sfemref_table.argtypes = [ctypes.c_int, ctypes.c_int] + [_dp] * 11
+        L.sfemref_save_table.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+        L.sfemref_load_table.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int] + [_dp] * 11
+        L.sfemref_tableset_get.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int] + [_dp] * 11
         L.sfemref_element.argtypes = [ctypes.c_int, _dp, _dp]
         L.sfemref_lines.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, _dp, _dp]
         L.sfemref_solve.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
@@ -74,21 +77,42 @@ def trig(kind: int, x: np.ndarray) -> np.ndarray:
     return y
 
 
-def table(n: int, K: int) -> dict:
+_TABLE_KEYS = ["theta", "half_cos", "half_sin", "values", "norm_sq", "nodal_weight", "p", "q", "interior_values",
+               "interior_vectors", "eig_coeff"]
+
+
+def _table_export(n: int, K: int, call) -> dict:
     m = n - 1
     out = dict(theta=np.empty(K - 1), half_cos=np.empty(K - 1), half_sin=np.empty(K - 1),
                values=np.empty((K - 1) * n), norm_sq=np.empty((K - 1) * n), nodal_weight=np.empty((K - 1) * n),
                p=np.empty(max(1, (K - 1) * n * m)), q=np.empty(max(1, (K - 1) * n * m)),
                interior_values=np.empty(max(1, m)), interior_vectors=np.empty(max(1, m * m)),
                eig_coeff=np.empty(n * K - 1))
-    keys = ["theta", "half_cos", "half_sin", "values", "norm_sq", "nodal_weight", "p", "q", "interior_values",
-            "interior_vectors", "eig_coeff"]
-    _chk(lib().sfemref_table(n, K, *[_p(out[k]) for k in keys]))
+    _chk(call(*[_p(out[k]) for k in _TABLE_KEYS]))
     for k in ("p", "q"):
         out[k] = out[k][:(K - 1) * n * m]
     out["interior_values"] = out["interior_values"][:m]
     out["interior_vectors"] = out["interior_vectors"][:m * m]
     return out
+
+
+def table(n: int, K: int) -> dict:
+    return _table_export(n, K, lambda *a: lib().sfemref_table(n, K, *a))
+
+
+def save_table(n: int, K: int, path: str):
+    """The reference's save_table (spectral.cpp:128-138) of its (n, K) table."""
+    _chk(lib().sfemref_save_table(n, K, path.encode()))
+
+
+def load_table(path: str, n: int, K: int) -> dict:
+    """The reference's load_table (spectral.cpp:152-236)."""
+    return _table_export(n, K, lambda *a: lib().sfemref_load_table(path.encode(), n, K, *a))
+
+
+def tableset_get(cache_dir: str, write_cache: bool, n: int, K: int) -> dict:
+    """TableSet(Double, cache_dir, write_cache).get(n, K) (poisson.cpp:49-73)."""
+    return _table_export(n, K, lambda *a: lib().sfemref_tableset_get(cache_dir.encode(), int(write_cache), n, K, *a))
 
 
 def element(n: int):

@@ -28,7 +28,8 @@ __all__ = [
     "SolveReport", "Plan", "GridFunction1D", "CoefficientArray1D", "GridFunctionND", "solve_with_load",
     "solve_dof", "synthesize", "decompose", "decompose_weighted", "lines", "lines_device", "DECOMPOSE_WEIGHTED",
     "DECOMPOSE", "SYNTHESIZE", "default_context", "HEADER_SYMBOLS", "Field", "solve", "FIELD_CONSTANT",
-    "FIELD_SINES", "FIELD_SIN1D", "FIELD_POISSON2D", "FIELD_POISSON3D", "CASE_FIELDS",
+    "FIELD_SINES", "FIELD_SIN1D", "FIELD_POISSON2D", "FIELD_POISSON3D", "CASE_FIELDS", "TABLE_TEXT",
+    "TABLE_BINARY", "build_and_save_table", "read_table_file",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -73,6 +74,12 @@ _SIGS = [
     ("sfem_cuda_table_create", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
     ("sfem_cuda_table_destroy", ctypes.c_int, [_vp]),
     ("sfem_cuda_table_export", ctypes.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    ("sfem_cuda_ctx_set_table_cache", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int]),
+    ("sfem_cuda_table_load", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("sfem_cuda_table_save", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int]),
+    ("sfem_cuda_table_file_build", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int]),
+    ("sfem_cuda_table_file_read", ctypes.c_int,
+     [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp, _dp, _dp]),
     ("sfem_cuda_lines_device", ctypes.c_int,
      [_vp, ctypes.c_int, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp]),
     ("sfem_cuda_lines_host", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_longlong, _dp, _dp]),
@@ -145,6 +152,13 @@ class Context:
         _check(lib.sfem_cuda_ctx_stream(self.handle, ctypes.byref(s)))
         return s.value or 0
 
+    def set_table_cache(self, cache_dir: Optional[str], write_cache: bool = True, binary: bool = True):
+        """TableSet's cache directory (poisson.hpp:50-52, poisson.cpp:49-73) for every later table of
+        this context: sfem_table_n<n>_K<K>.bin, then the reference's .txt, are tried; an absent or
+        stale entry is rebuilt and (write_cache) written, binary or in the reference's SFEM1 text."""
+        flags = (1 if write_cache else 0) | (2 if binary else 0)
+        _check(lib.sfem_cuda_ctx_set_table_cache(self.handle, (cache_dir or "").encode(), flags))
+
     def close(self):
         if self.handle:
             lib.sfem_cuda_ctx_destroy(self.handle)
@@ -167,34 +181,73 @@ def default_context() -> Context:
     return _DEFAULT
 
 
+TABLE_TEXT, TABLE_BINARY = 0, 1  # SFEM1 (the reference's text format) / SFEMB1 (raw doubles + checksum)
+
+
+def _table_arrays(n: int, K: int) -> dict:
+    m = n - 1
+    return dict(values=np.empty((K - 1) * n), norm_sq=np.empty((K - 1) * n),
+                p=np.empty(max(1, (K - 1) * n * m)), interior_values=np.empty(max(1, m)),
+                interior_vectors=np.empty(max(1, m * m)), eig_coeff=np.empty(n * K - 1))
+
+
+_EXPORT_KEYS = ("values", "norm_sq", "p", "interior_values", "interior_vectors", "eig_coeff")
+
+
+def _trim(out: dict, n: int, K: int) -> dict:
+    m = n - 1
+    out["p"] = out["p"][:(K - 1) * n * m]
+    out["interior_values"] = out["interior_values"][:m]
+    out["interior_vectors"] = out["interior_vectors"][:m * m]
+    return out
+
+
+def build_and_save_table(order: int, elements: int, path: str, fmt: int = TABLE_TEXT):
+    """build_and_save_table (spectral.hpp:320, spectral.cpp:140-150) on the host (no device)."""
+    _check(lib.sfem_cuda_table_file_build(order, elements, os.fspath(path).encode(), fmt))
+
+
+def read_table_file(path: str, order: int, elements: int) -> dict:
+    """load_table (spectral.cpp:152-236) on the host, returning the primaries as table.export() does."""
+    out = _table_arrays(order, elements)
+    _check(lib.sfem_cuda_table_file_read(os.fspath(path).encode(), order, elements,
+                                         *[_dptr(out[k]) for k in _EXPORT_KEYS]))
+    return _trim(out, order, elements)
+
+
 class SpectralTable:
     """Device spectral table for one (order, elements) (SpectralTable1D, spectral.hpp:281-312)."""
 
-    def __init__(self, order: int, elements: int, ctx: Optional[Context] = None):
+    def __init__(self, order: int, elements: int, ctx: Optional[Context] = None, _handle=None):
         self.ctx = ctx or default_context()
-        h = _vp()
-        _check(lib.sfem_cuda_table_create(self.ctx.handle, order, elements, ctypes.byref(h)))
+        h = _handle
+        if h is None:
+            h = _vp()
+            _check(lib.sfem_cuda_table_create(self.ctx.handle, order, elements, ctypes.byref(h)))
         self.handle = h
         self.order = order
         self.elements = elements
+
+    @classmethod
+    def load(cls, path: str, order: int, elements: int, ctx: Optional[Context] = None) -> "SpectralTable":
+        """load_table (spectral.hpp:326): SFEM1 text (the reference's files) or SFEMB1 binary."""
+        ctx = ctx or default_context()
+        h = _vp()
+        _check(lib.sfem_cuda_table_load(ctx.handle, os.fspath(path).encode(), order, elements, ctypes.byref(h)))
+        return cls(order, elements, ctx, _handle=h)
+
+    def save(self, path: str, fmt: int = TABLE_TEXT):
+        """save_table (spectral.hpp:325); TABLE_TEXT writes the reference's file byte for byte."""
+        _check(lib.sfem_cuda_table_save(self.handle, os.fspath(path).encode(), fmt))
 
     @property
     def coeff_count(self) -> int:
         return self.order * self.elements - 1
 
     def export(self) -> dict:
-        n, K = self.order, self.elements
-        m = n - 1
-        out = dict(values=np.empty((K - 1) * n), norm_sq=np.empty((K - 1) * n),
-                   p=np.empty(max(1, (K - 1) * n * m)), interior_values=np.empty(max(1, m)),
-                   interior_vectors=np.empty(max(1, m * m)), eig_coeff=np.empty(n * K - 1))
-        _check(lib.sfem_cuda_table_export(self.handle, *[_dptr(out[k]) for k in
-                                                         ("values", "norm_sq", "p", "interior_values",
-                                                          "interior_vectors", "eig_coeff")]))
-        out["p"] = out["p"][:(K - 1) * n * m]
-        out["interior_values"] = out["interior_values"][:m]
-        out["interior_vectors"] = out["interior_vectors"][:m * m]
-        return out
+        out = _table_arrays(self.order, self.elements)
+        _check(lib.sfem_cuda_table_export(self.handle, *[_dptr(out[k]) for k in _EXPORT_KEYS]))
+        return _trim(out, self.order, self.elements)
 
     def eigenvalues_coeff_order(self) -> np.ndarray:
         return self.export()["eig_coeff"]
@@ -209,11 +262,18 @@ class SpectralTable:
 
 
 class TableSet:
-    """Tables keyed by (order, elements), built on demand (TableSet, poisson.hpp:48-62)."""
+    """Tables keyed by (order, elements), built on demand (TableSet, poisson.hpp:48-62).
 
-    def __init__(self, ctx: Optional[Context] = None):
+    cache_dir / write_cache follow the reference's constructor (poisson.hpp:50-52): tables are
+    looked up on disk first (the reference's sfem_table_n<n>_K<K>.txt, or our .bin) and rebuilt
+    when absent or stale.  The cache is set on the context, so plans built on it use it too."""
+
+    def __init__(self, ctx: Optional[Context] = None, cache_dir: Optional[str] = None, write_cache: bool = False,
+                 binary: bool = True):
         self.ctx = ctx or default_context()
         self._tables = {}
+        if cache_dir:
+            self.ctx.set_table_cache(os.fspath(cache_dir), write_cache, binary)
 
     def get(self, order: int, elements: int) -> SpectralTable:
         key = (order, elements)

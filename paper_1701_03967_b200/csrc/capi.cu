@@ -100,6 +100,7 @@ struct sfem_ctx_s {
   cudaStream_t stream = nullptr;
   double* scratch = nullptr;
   size_t scratch_doubles = 0;
+  TableCache table_cache;  // TableSet's cache directory (poisson.cpp:49-73); empty = none
 };
 
 struct sfem_table_s {
@@ -1111,9 +1112,61 @@ int sfem_cuda_table_create(sfem_ctx ctx, int order, int elements, sfem_table* ou
     require(ctx && out, "table_create: null argument");
     auto t = std::make_unique<sfem_table_s>();
     t->ctx = ctx;
-    t->host = build_host_table(order, elements);
+    t->host = cached_host_table(ctx->table_cache, order, elements);
     upload_table(t.get());
     *out = t.release();
+  });
+}
+
+int sfem_cuda_ctx_set_table_cache(sfem_ctx ctx, const char* dir, int flags) {
+  return guarded([&] {
+    require(ctx != nullptr, "set_table_cache: null context");
+    require((flags & ~3) == 0, "set_table_cache: unknown flags");
+    ctx->table_cache.dir = dir ? dir : "";
+    ctx->table_cache.write = (flags & SFEM_TABLE_CACHE_WRITE) != 0;
+    ctx->table_cache.format = (flags & SFEM_TABLE_CACHE_BINARY) ? kTableBinary : kTableText;
+  });
+}
+
+int sfem_cuda_table_load(sfem_ctx ctx, const char* path, int order, int elements, sfem_table* out) {
+  return guarded([&] {
+    require(ctx && path && out, "table_load: null argument");
+    auto t = std::make_unique<sfem_table_s>();
+    t->ctx = ctx;
+    t->host = load_host_table(path, order, elements);
+    upload_table(t.get());
+    *out = t.release();
+  });
+}
+
+int sfem_cuda_table_save(sfem_table t, const char* path, int format) {
+  return guarded([&] {
+    require(t && path, "table_save: null argument");
+    save_host_table(t->host, path, format);
+  });
+}
+
+int sfem_cuda_table_file_build(int order, int elements, const char* path, int format) {
+  return guarded([&] {
+    require(path != nullptr, "build_and_save_table: null path");
+    save_host_table(build_host_table(order, elements), path, format);
+  });
+}
+
+int sfem_cuda_table_file_read(const char* path, int order, int elements, double* values, double* norm_sq,
+                              double* p, double* interior_values, double* interior_vectors, double* eig_coeff) {
+  return guarded([&] {
+    require(path != nullptr, "load_table: null path");
+    const HostTable h = load_host_table(path, order, elements);
+    auto cp = [](const std::vector<double>& v, double* dst) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(h.values, values);
+    cp(h.norm_sq, norm_sq);
+    cp(h.p, p);
+    cp(h.interior_values, interior_values);
+    cp(h.interior_vectors, interior_vectors);
+    cp(h.eig_coeff, eig_coeff);
   });
 }
 
@@ -1230,7 +1283,7 @@ int sfem_cuda_plan_create(sfem_ctx ctx, int dim, const int* orders, const int* e
       if (it == cache.end()) {
         auto t = std::make_unique<sfem_table_s>();
         t->ctx = ctx;
-        t->host = build_host_table(orders[i], elements[i]);
+        t->host = cached_host_table(ctx->table_cache, orders[i], elements[i]);
         upload_table(t.get());
         it = cache.emplace(key, t.get()).first;
         p->owned.push_back(std::move(t));
@@ -1468,7 +1521,7 @@ int sfem_cuda_dist_create(sfem_ctx ctx, int dim, const int* orders, const int* e
       if (it == cache.end()) {
         auto t = std::make_unique<sfem_table_s>();
         t->ctx = ctx;
-        t->host = build_host_table(orders[i], elements[i]);
+        t->host = cached_host_table(ctx->table_cache, orders[i], elements[i]);
         upload_table(t.get());
         it = cache.emplace(key, t.get()).first;
         d->owned.push_back(std::move(t));
@@ -1803,7 +1856,7 @@ int sfem_cuda_peer_create(sfem_ctx ctx, int dim, const int* orders, const int* e
       if (it == cache.end()) {
         auto t = std::make_unique<sfem_table_s>();
         t->ctx = ctx;
-        t->host = build_host_table(orders[i], elements[i]);
+        t->host = cached_host_table(ctx->table_cache, orders[i], elements[i]);
         upload_table(t.get());
         it = cache.emplace(key, t.get()).first;
         d->owned.push_back(std::move(t));

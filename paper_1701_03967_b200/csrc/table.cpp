@@ -6,6 +6,13 @@
 #include "table.hpp"
 
 #include <algorithm>
+#include <charconv>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+
+#include <unistd.h>
 #include <cmath>
 #include <limits>
 #include <stdexcept>
@@ -551,56 +558,13 @@ void load_quadrature(int n, std::vector<double>& nodes, std::vector<double>& wei
     for (int g = 0; g <= n; ++g) weighted[static_cast<size_t>(loc) * (n + 1) + g] = w[g] * lagrange_value(eq, loc, nodes[g]);
 }
 
-HostTable build_host_table(int n, int K) {
-  if (K < 2) fail("spectral table: need at least two elements");
-  const Element em = build_element(n);
-  Interior es;
-  if (n >= 2) es = interior_eigensystem(em);
-  const int m = n - 1;
-  HostTable t;
-  t.order = n;
-  t.elements = K;
-  t.stiffness = em.stiffness.a;
-  t.mass = em.mass.a;
-  t.mass_interior = em.mb.interior.a;
-  t.interior_values = es.values;
-  t.interior_vectors = es.vectors.a;
-  t.theta.resize(K - 1);
-  t.values.resize(static_cast<size_t>(K - 1) * n);
-  t.norm_sq.resize(t.values.size());
-  t.p.resize(t.values.size() * m);
-  const Blocks& mb = em.mb;
-  const double pi = std::acos(-1.0);
-  for (int k = 1; k < K; ++k) {
-    const double theta = std::cos(pi * static_cast<double>(k) / static_cast<double>(K));
-    t.theta[k - 1] = theta;
-    const std::vector<double> roots = solve_theta(es, em, theta);
-    for (int l = 1; l <= n; ++l) {
-      const double lambda = roots[l - 1];
-      const size_t idx = static_cast<size_t>(k - 1) * n + (l - 1);
-      t.values[idx] = lambda;
-      std::vector<double> p(m);
-      if (m > 0) p = interior_solution(es, n, lambda);
-      for (int i = 0; i < m; ++i) t.p[idx * m + i] = p[i];
-      std::vector<double> cp(m, 0.0);
-      for (int i = 0; i < m; ++i) {
-        double s = 0;
-        for (int j = 0; j < m; ++j) s += mb.interior(i, j) * p[j];
-        cp[i] = s;
-      }
-      double term_direct = mb.corner, term_rev = mb.cross;
-      for (int i = 0; i < m; ++i) {
-        const double w = cp[i] + 2 * mb.edge[i];
-        term_direct += w * p[i];
-        term_rev += w * p[m - 1 - i];
-      }
-      const double norm_sq = static_cast<double>(K) * (term_direct + theta * term_rev);
-      if (!(norm_sq > 0))
-        fail("spectral table: nonpositive squared norm at k=" + std::to_string(k) + " l=" + std::to_string(l));
-      t.norm_sq[idx] = norm_sq;
-    }
-  }
-  // finalize_table (spectral.cpp:21-79)
+namespace {
+
+// finalize_table (spectral.cpp:21-79): the per-frequency data derived from the
+// primaries (theta, values, p, norm_sq).  Shared by the builder and the file
+// loaders, as in the reference (spectral.cpp:112, 235).
+void finalize_host_table(HostTable& t, const Blocks& mb) {
+  const int n = t.order, K = t.elements, m = n - 1;
   t.half_cos.resize(K - 1);
   t.half_sin.resize(K - 1);
   for (int k = 1; k < K; ++k) {
@@ -625,8 +589,322 @@ HostTable build_host_table(int n, int K) {
     t.nodal_weight[idx] = 2.0 * (mb.corner + edge_dot + theta * (mb.cross + edge_dot_rev));
   }
   t.eig_coeff.clear();
-  for (int l = 0; l < m; ++l) t.eig_coeff.push_back(es.values[l]);
+  t.eig_coeff.reserve(static_cast<size_t>(n) * K - 1);
+  for (int l = 0; l < m; ++l) t.eig_coeff.push_back(t.interior_values[l]);
   for (size_t idx = 0; idx < pairs; ++idx) t.eig_coeff.push_back(t.values[idx]);
+}
+
+// Element data and the sized per-k arrays shared by the builder and the loaders.
+HostTable table_skeleton(const Element& em, int K) {
+  const int n = em.n, m = n - 1;
+  HostTable t;
+  t.order = n;
+  t.elements = K;
+  t.stiffness = em.stiffness.a;
+  t.mass = em.mass.a;
+  t.mass_interior = em.mb.interior.a;
+  t.interior_values.assign(m, 0.0);
+  t.interior_vectors.assign(static_cast<size_t>(m) * m, 0.0);
+  t.theta.resize(K - 1);
+  const double pi = std::acos(-1.0);
+  for (int k = 1; k < K; ++k) t.theta[k - 1] = std::cos(pi * static_cast<double>(k) / static_cast<double>(K));
+  t.values.resize(static_cast<size_t>(K - 1) * n);
+  t.norm_sq.resize(t.values.size());
+  t.p.resize(t.values.size() * m);
+  return t;
+}
+
+}  // namespace
+
+HostTable build_host_table(int n, int K) {
+  if (K < 2) fail("spectral table: need at least two elements");
+  const Element em = build_element(n);
+  Interior es;
+  if (n >= 2) es = interior_eigensystem(em);
+  const int m = n - 1;
+  HostTable t = table_skeleton(em, K);
+  t.interior_values = es.values;
+  t.interior_vectors = es.vectors.a;
+  const Blocks& mb = em.mb;
+  // The reference builds frequency by frequency on one thread
+  // (spectral.hpp:228-277); every k is independent (one theta-equation root
+  // solve and n interior solutions), so the cold build runs them in parallel.
+  // A failure reports the lowest failing k, as the serial loop would.
+  int bad_k = K;
+  std::string bad_msg;
+#pragma omp parallel for schedule(dynamic, 4) if (K > 64)
+  for (int k = 1; k < K; ++k) {
+    try {
+      const double theta = t.theta[k - 1];
+      const std::vector<double> roots = solve_theta(es, em, theta);
+      for (int l = 1; l <= n; ++l) {
+        const double lambda = roots[l - 1];
+        const size_t idx = static_cast<size_t>(k - 1) * n + (l - 1);
+        t.values[idx] = lambda;
+        std::vector<double> p(m);
+        if (m > 0) p = interior_solution(es, n, lambda);
+        for (int i = 0; i < m; ++i) t.p[idx * m + i] = p[i];
+        std::vector<double> cp(m, 0.0);
+        for (int i = 0; i < m; ++i) {
+          double s = 0;
+          for (int j = 0; j < m; ++j) s += mb.interior(i, j) * p[j];
+          cp[i] = s;
+        }
+        double term_direct = mb.corner, term_rev = mb.cross;
+        for (int i = 0; i < m; ++i) {
+          const double w = cp[i] + 2 * mb.edge[i];
+          term_direct += w * p[i];
+          term_rev += w * p[m - 1 - i];
+        }
+        const double norm_sq = static_cast<double>(K) * (term_direct + theta * term_rev);
+        if (!(norm_sq > 0))
+          fail("spectral table: nonpositive squared norm at k=" + std::to_string(k) + " l=" + std::to_string(l));
+        t.norm_sq[idx] = norm_sq;
+      }
+    } catch (const std::exception& e) {
+#pragma omp critical(sfem_table_build_fail)
+      if (k < bad_k) {
+        bad_k = k;
+        bad_msg = e.what();
+      }
+    }
+  }
+  if (bad_k < K) fail(bad_msg);
+  finalize_host_table(t, mb);
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// Table files (reference save_table / load_table / build_and_save_table,
+// spectral.cpp:81-236) and the cache directory of TableSet (poisson.cpp:49-73).
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr char kBinaryMagic[8] = {'S', 'F', 'E', 'M', 'B', '1', '\0', '\0'};
+
+// format_records (spectral.cpp:81-105) at 17 significant digits: the k = 0
+// records carry (lambda0_l, e^(l), K), the others (lambda_kl, p_kl, ||s_kl||^2).
+std::string format_text(const HostTable& t) {
+  const int n = t.order, K = t.elements, m = n - 1;
+  std::string out = "SFEM1 " + std::to_string(n) + " " + std::to_string(K) + " 17\n";
+  out.reserve(out.size() + static_cast<size_t>(n) * K * (n + 4) * 25);
+  char buf[64];
+  auto num = [&](double v) {
+    std::snprintf(buf, sizeof buf, " %.*g", 17, v);
+    out += buf;
+  };
+  for (int l = 1; l <= m; ++l) {
+    out += "0 " + std::to_string(l);
+    num(t.interior_values[l - 1]);
+    for (int i = 0; i < m; ++i) num(t.interior_vectors[static_cast<size_t>(i) * m + (l - 1)]);
+    num(static_cast<double>(K));
+    out += '\n';
+  }
+  for (int k = 1; k < K; ++k)
+    for (int l = 1; l <= n; ++l) {
+      const size_t idx = static_cast<size_t>(k - 1) * n + (l - 1);
+      out += std::to_string(k) + " " + std::to_string(l);
+      num(t.values[idx]);
+      for (int i = 0; i < m; ++i) num(t.p[idx * m + i]);
+      num(t.norm_sq[idx]);
+      out += '\n';
+    }
+  return out;
+}
+
+uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < bytes; ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h;
+}
+
+// The primaries in file order: interior values, interior vectors (row-major
+// [i][l-1]), then per (k, l) values, norm_sq, p.
+std::vector<std::vector<double>*> binary_parts(HostTable& t) {
+  return {&t.interior_values, &t.interior_vectors, &t.values, &t.norm_sq, &t.p};
+}
+
+std::string read_file(const std::string& path) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) fail("load_table: cannot open '" + path + "'");
+  std::string s;
+  char buf[1 << 16];
+  size_t got;
+  while ((got = std::fread(buf, 1, sizeof buf, f)) > 0) s.append(buf, got);
+  std::fclose(f);
+  return s;
+}
+
+void write_file(const std::string& path, const std::string& data) {
+  // Write to a temporary name and rename, so a concurrent reader of the cache
+  // never sees a partial file (the reference writes in place, spectral.cpp:117-124).
+  static std::atomic<int> serial{0};
+  const std::string tmp = path + ".tmp" + std::to_string(static_cast<long long>(getpid())) + "_" +
+                          std::to_string(serial.fetch_add(1));
+  std::FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) fail("save_table: cannot open '" + path + "' for writing");
+  const bool ok = std::fwrite(data.data(), 1, data.size(), f) == data.size();
+  if (std::fclose(f) != 0 || !ok || std::rename(tmp.c_str(), path.c_str()) != 0) {
+    std::remove(tmp.c_str());
+    fail("save_table: write failed for '" + path + "'");
+  }
+}
+
+struct Tokens {
+  const char* p;
+  const char* end;
+  void skip() {
+    while (p < end && (*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r')) ++p;
+  }
+  bool word(std::string& w) {
+    skip();
+    const char* s = p;
+    while (p < end && !(*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r')) ++p;
+    w.assign(s, p);
+    return p > s;
+  }
+  bool integer(int& v) {
+    skip();
+    auto r = std::from_chars(p, end, v);
+    if (r.ec != std::errc()) return false;
+    p = r.ptr;
+    return true;
+  }
+  bool real(double& v) {
+    skip();
+    auto r = std::from_chars(p, end, v);
+    if (r.ec != std::errc()) return false;
+    p = r.ptr;
+    return true;
+  }
+};
+
+void check_header(int fn, int fk, int n, int K) {
+  if (fn != n || fk != K)
+    fail("load_table: file holds order " + std::to_string(fn) + ", elements " + std::to_string(fk) +
+         " but order " + std::to_string(n) + ", elements " + std::to_string(K) + " were requested");
+  if (!(n >= 1 && K >= 2 && n <= 9)) fail("load_table: header values out of range");
+}
+
+HostTable parse_text(const std::string& s, const std::string& path, int n, int K) {
+  Tokens in{s.data(), s.data() + s.size()};
+  std::string magic;
+  int fn = 0, fk = 0, digits = 0;
+  if (!(in.word(magic) && in.integer(fn) && in.integer(fk) && in.integer(digits)))
+    fail("load_table: malformed header in '" + path + "'");
+  if (magic != "SFEM1") fail("load_table: unsupported format '" + magic + "' in '" + path + "'");
+  check_header(fn, fk, n, K);
+  const int m = n - 1;
+  HostTable t = table_skeleton(build_element(n), K);
+  const size_t expected = static_cast<size_t>(n) * K - 1;
+  std::vector<double> vec(m);
+  for (size_t rec = 0; rec < expected; ++rec) {
+    int k = 0, l = 0;
+    double lambda = 0, norm = 0;
+    if (!(in.integer(k) && in.integer(l) && in.real(lambda)))
+      fail("load_table: truncated or corrupt record " + std::to_string(rec + 1) + " in '" + path + "'");
+    for (int i = 0; i < m; ++i)
+      if (!in.real(vec[i])) fail("load_table: truncated interior vector in record " + std::to_string(rec + 1));
+    if (!in.real(norm)) fail("load_table: truncated record " + std::to_string(rec + 1));
+    if (k == 0) {
+      if (l < 1 || l > m) fail("load_table: zero-frequency record with bad index");
+      t.interior_values[l - 1] = lambda;
+      for (int i = 0; i < m; ++i) t.interior_vectors[static_cast<size_t>(i) * m + (l - 1)] = vec[i];
+    } else {
+      if (k < 1 || k >= K || l < 1 || l > n) fail("load_table: record index out of range");
+      const size_t idx = static_cast<size_t>(k - 1) * n + (l - 1);
+      t.values[idx] = lambda;
+      for (int i = 0; i < m; ++i) t.p[idx * m + i] = vec[i];
+      t.norm_sq[idx] = norm;
+    }
+  }
+  std::string trailing;
+  if (in.word(trailing)) fail("load_table: unexpected trailing data in '" + path + "'");
+  return t;
+}
+
+HostTable parse_binary(const std::string& s, const std::string& path, int n, int K) {
+  struct Header {
+    char magic[8];
+    int32_t order, elements, digits, reserved;
+    uint64_t count;
+  } h;
+  if (s.size() < sizeof h) fail("load_table: malformed header in '" + path + "'");
+  std::memcpy(&h, s.data(), sizeof h);
+  check_header(h.order, h.elements, n, K);
+  const int m = n - 1;
+  HostTable t = table_skeleton(build_element(n), K);
+  size_t count = 0;
+  for (auto* v : binary_parts(t)) count += v->size();
+  if (h.count != count || s.size() != sizeof h + count * sizeof(double) + sizeof(uint64_t))
+    fail("load_table: truncated or corrupt payload in '" + path + "'");
+  const char* p = s.data() + sizeof h;
+  uint64_t sum;
+  std::memcpy(&sum, p + count * sizeof(double), sizeof sum);
+  if (sum != fnv1a(p, count * sizeof(double))) fail("load_table: checksum mismatch in '" + path + "'");
+  for (auto* v : binary_parts(t)) {
+    std::memcpy(v->data(), p, v->size() * sizeof(double));
+    p += v->size() * sizeof(double);
+  }
+  (void)m;
+  return t;
+}
+
+}  // namespace
+
+void save_host_table(const HostTable& t, const std::string& path, int format) {
+  if (format == kTableText) {
+    write_file(path, format_text(t));
+    return;
+  }
+  if (format != kTableBinary) fail("save_table: unknown format " + std::to_string(format));
+  HostTable c = t;  // binary_parts wants mutable vectors
+  size_t count = 0;
+  for (auto* v : binary_parts(c)) count += v->size();
+  std::string out(sizeof(kBinaryMagic) + 4 * sizeof(int32_t) + sizeof(uint64_t), '\0');
+  char* w = out.data();
+  std::memcpy(w, kBinaryMagic, sizeof kBinaryMagic);
+  const int32_t hdr[4] = {t.order, t.elements, 17, 0};
+  std::memcpy(w + 8, hdr, sizeof hdr);
+  const uint64_t cnt = count;
+  std::memcpy(w + 24, &cnt, sizeof cnt);
+  const size_t payload_at = out.size();
+  for (auto* v : binary_parts(c)) out.append(reinterpret_cast<const char*>(v->data()), v->size() * sizeof(double));
+  const uint64_t sum = fnv1a(out.data() + payload_at, count * sizeof(double));
+  out.append(reinterpret_cast<const char*>(&sum), sizeof sum);
+  write_file(path, out);
+}
+
+HostTable load_host_table(const std::string& path, int n, int K) {
+  const std::string s = read_file(path);
+  HostTable t = (s.size() >= 8 && std::memcmp(s.data(), kBinaryMagic, 8) == 0) ? parse_binary(s, path, n, K)
+                                                                                  : parse_text(s, path, n, K);
+  // the reference rebuilds the derived data after a load (spectral.cpp:209-235)
+  finalize_host_table(t, build_element(n).mb);
+  return t;
+}
+
+std::string table_cache_path(const std::string& dir, int n, int K, int format) {
+  return dir + "/sfem_table_n" + std::to_string(n) + "_K" + std::to_string(K) +
+         (format == kTableBinary ? ".bin" : ".txt");
+}
+
+HostTable cached_host_table(const TableCache& cache, int n, int K, int* source) {
+  if (source) *source = 0;
+  if (cache.dir.empty()) return build_host_table(n, K);
+  // TableSet::get (poisson.cpp:49-73): a stale or unreadable entry is rebuilt.
+  // The binary entry is tried first, then the reference's text entry, so a
+  // cache directory the reference filled is used as is.
+  for (int format : {kTableBinary, kTableText}) {
+    try {
+      HostTable t = load_host_table(table_cache_path(cache.dir, n, K, format), n, K);
+      if (source) *source = 1 + format;
+      return t;
+    } catch (const std::exception&) {
+    }
+  }
+  HostTable t = build_host_table(n, K);
+  if (cache.write) save_host_table(t, table_cache_path(cache.dir, n, K, cache.format), cache.format);
   return t;
 }
 

@@ -58,6 +58,28 @@ struct DeviceTableData {
 
 DeviceTableData derive_device_data(const HostTable& t);
 
+// Table files (reference save_table / load_table / build_and_save_table,
+// spectral.hpp:316-330, spectral.cpp:81-236).  kTableText is the reference's
+// SFEM1 text format, written byte for byte as the reference writes it (17
+// significant digits) and read as the reference reads it; kTableBinary
+// ("SFEMB1") carries the same primaries as raw doubles with an FNV-1a
+// checksum (bit-exact, no text parse).  Loading sniffs the format and
+// rebuilds the derived data (spectral.cpp:209-235).  Errors throw
+// std::runtime_error with the reference's messages.
+enum { kTableText = 0, kTableBinary = 1 };
+void save_host_table(const HostTable& t, const std::string& path, int format);
+HostTable load_host_table(const std::string& path, int n, int K);
+
+// TableSet's on-disk cache (poisson.cpp:49-73): `dir` empty = no cache.
+struct TableCache {
+  std::string dir;
+  bool write = true;
+  int format = kTableBinary;
+};
+std::string table_cache_path(const std::string& dir, int n, int K, int format);
+// source (optional): 0 built, 1 loaded from the text entry, 2 from the binary one.
+HostTable cached_host_table(const TableCache& cache, int n, int K, int* source = nullptr);
+
 // Gauss nodes (n+1 points) and weighted[loc*(n+1)+g] = w_g phi_loc(xi_g) of the
 // load averaging (reference axis_quad, poisson.cpp:481-495).
 void load_quadrature(int n, std::vector<double>& nodes, std::vector<double>& weighted);

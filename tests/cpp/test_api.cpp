@@ -3,6 +3,8 @@
 // test_poisson.cpp).  Built and run by tests/test_cpp_api.py (GPU).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <random>
 #include <vector>
 
@@ -292,8 +294,44 @@ static void partial_matches_full(TableSet& tables) {
   CHECK(w <= 1e-12 * nrm);
 }
 
+// Table files and the cache directory (spectral.cpp:81-236, poisson.cpp:49-73):
+// a table saved and loaded back in either format transforms bit for bit like
+// the built one; a second TableSet over the same directory loads the entry;
+// a file for another (n, K) is refused with load_table's message.
+static void table_files() {
+  Context& ctx = default_context();
+  const std::string dir = std::string(std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp") + "/sfem_cpp_tables_" +
+                          std::to_string(static_cast<long long>(std::random_device{}()));
+  std::system(("mkdir -p " + dir).c_str());
+  SpectralTable built(ctx, 4, 24);
+  const GridFunction1D g = random_grid(4, 24, 11);
+  const std::vector<double> want = decompose_weighted(g, built).data;
+  for (TableFormat f : {TableFormat::Text, TableFormat::Binary}) {
+    const std::string path = dir + (f == TableFormat::Text ? "/t.txt" : "/t.bin");
+    built.save(path, f);
+    auto loaded = SpectralTable::load(ctx, path, 4, 24);
+    CHECK(max_diff(decompose_weighted(g, *loaded).data, want) == 0.0);
+    CHECK(loaded->eigenvalues_coeff_order() == built.eigenvalues_coeff_order());
+    CHECK_THROWS(SpectralTable::load(ctx, path, 4, 25));
+  }
+  build_and_save_table(3, 10, dir + "/sfem_table_n3_K10.txt");
+  {
+    Context c2(0);
+    TableSet cached(c2, dir, true, TableFormat::Binary);
+    const auto& t = cached.get(3, 10);  // loads the text entry
+    SpectralTable fresh(ctx, 3, 10);
+    CHECK(t.eigenvalues_coeff_order() == fresh.eigenvalues_coeff_order());
+    cached.get(5, 12);  // built, then written as .bin
+  }
+  std::FILE* f = std::fopen((dir + "/sfem_table_n5_K12.bin").c_str(), "rb");
+  CHECK(f != nullptr);
+  if (f) std::fclose(f);
+  std::system(("rm -rf " + dir).c_str());
+}
+
 int main() {
   TableSet tables;
+  table_files();
   roundtrip_identities(tables);
   dimension_mismatches(tables);
   solve_vs_dense(tables);
