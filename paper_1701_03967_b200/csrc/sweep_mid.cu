@@ -27,6 +27,9 @@
 #ifndef SFEM_MID_R16
 #define SFEM_MID_R16 1
 #endif
+#ifndef SFEM_MID_KMIX
+#define SFEM_MID_KMIX 1
+#endif
 
 namespace sfem_b200 {
 namespace mid {
@@ -416,12 +419,24 @@ __device__ __forceinline__ void forward_post(const double2* Z, double* R, const 
 //   MODE kInverse:             u = Mi c
 //   MODE kForwardDivideInverse u = Mi (Mf v / denom)
 // Items (K-1)*B .. (K-1)*B + B - 1 are the centre blocks of the lines.
+//
+// SFEM_MID_KMIX (default): the matrices are the k-contiguous copies mixT_w/d
+// ([l][s][k]) and mixT_i ([s][l][k]).  Items run b-fastest, so a warp covers
+// 32/B consecutive frequencies and one matrix load is one or a few 32-byte
+// sectors instead of 32/B of them (the per-frequency [k][l][s] layout).
+// C3 (n=9, K=1024: 0.66 MB per matrix set, not L1-resident): solve 8.30 ->
+// 4.92 ms; C5 n=4 / n=9: -6 % / -5 % (bitwise-identical results).
 template <class C, int MODE>
 __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, const double* __restrict__ mixF,
                                     const double* __restrict__ e0F, const double* __restrict__ mixI,
                                     const double* __restrict__ e0I, const double* base,
                                     const double* __restrict__ eig, double f_last) {
   constexpr int N = C::N, n = C::n, m = C::m, B = C::B;
+#if SFEM_MID_KMIX
+#define MIDX(a, b) (((a) * n + (b)) * N)
+#else
+#define MIDX(a, b) ((a) * n + (b))
+#endif
   constexpr int ITEMS = (N - 1) * B + B;
   for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
     if (it < (N - 1) * B) {
@@ -432,12 +447,17 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 #pragma unroll
       for (int s = 0; s < n; ++s) v[s] = pin[s * C::PSTR];
       if (MODE != kInverse) {
+#if SFEM_MID_KMIX
+        const double* M = mixF + k;
+        v[0] *= 2.0;  // the nodal column of mixT_* carries a factor 1/2 (exact)
+#else
         const double* M = mixF + static_cast<size_t>(k - 1) * n * n;
+#endif
 #pragma unroll
         for (int l = 0; l < n; ++l) {
           double acc = 0.0;
 #pragma unroll
-          for (int s = 0; s < n; ++s) acc = fma(__ldg(M + l * n + s), v[s], acc);
+          for (int s = 0; s < n; ++s) acc = fma(__ldg(M + MIDX(l, s)), v[s], acc);
           if (MODE == kForwardDivideInverse) acc = acc / (base[b] + f_last * __ldg(eig + m + (k - 1) * n + l));
           c[l] = acc;
         }
@@ -446,14 +466,21 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
         for (int l = 0; l < n; ++l) c[l] = v[l];
       }
       if (MODE != kForward) {
+#if SFEM_MID_KMIX
+        const double* M = mixI + k;
+#else
         const double* M = mixI + static_cast<size_t>(k - 1) * n * n;
+#endif
 #pragma unroll
         for (int s = 0; s < n; ++s) {
           double acc = 0.0;
 #pragma unroll
-          for (int l = 0; l < n; ++l) acc = fma(__ldg(M + s * n + l), c[l], acc);
+          for (int l = 0; l < n; ++l) acc = fma(__ldg(M + MIDX(s, l)), c[l], acc);
           v[s] = acc;
         }
+#if SFEM_MID_KMIX
+        v[0] *= 2.0;  // nodal row of mixT_i carries 1/2 (exact)
+#endif
 #pragma unroll
         for (int s = 0; s < n; ++s) p[s * C::PSTR] = v[s];
       } else {
@@ -494,6 +521,8 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
   }
   __syncthreads();
 }
+
+#undef MIDX
 
 // ------------------------------------------------------------ inverse fill
 template <class C>
@@ -701,7 +730,7 @@ __global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)  // 256-thread tiles: t
     forward_post<C>(reinterpret_cast<const double2*>(R), R, t.mk);
   }
   SFEM_PT(2);
-  mix<C, MODE>(R, R, C0, mixF, e0F, t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
   SFEM_PT(3);
   if (MODE != kForward) {
     inverse_fill<C>(R, reinterpret_cast<double2*>(R), t.mkh, t.om);
@@ -792,7 +821,7 @@ __global__ void __launch_bounds__(TH, 1)
     centre_reduce<C>(PS, C0);
     forward_post<C, true>(Z, R, t.mk);
   }
-  mix<C, MODE>(R, R, C0, mixF, e0F, t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
   if (MODE != kForward) {
     inverse_fill<C, true>(R, W0, t.mkh, t.om);
     const double2* Z = fft_oop<C>(W0, W1, t.tw);
@@ -818,7 +847,8 @@ __global__ void __launch_bounds__(TH, 1)
 template <int NN, int K, int BB, int TH>
 cudaError_t launch_gw(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
                       double* gwork, cudaStream_t stream) {
-  const double* mixF = analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w;
+  const double* mixF = SFEM_MID_KMIX ? (analysis == kDirect ? t.mixT_d : t.mixT_w)
+                                     : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
   const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
   SymbolInfo s{};
   if (sym) s = *sym;
@@ -848,7 +878,8 @@ cudaError_t launch_gw(const DevTable& t, const LineSet& ls, int mode, int analys
 template <int NN, int K, int BB, int TH>
 cudaError_t launch(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
                    cudaStream_t stream) {
-  const double* mixF = analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w;
+  const double* mixF = SFEM_MID_KMIX ? (analysis == kDirect ? t.mixT_d : t.mixT_w)
+                                     : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
   const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
   SymbolInfo s{};
   if (sym) s = *sym;
