@@ -222,9 +222,37 @@ inline CoefficientArray1D decompose_weighted(const GridFunction1D& y, const Spec
   return c;
 }
 
-inline CoefficientArray1D decompose(const GridFunction1D& w, const SpectralTable& table) {
+// apply_mass_1d / apply_stiffness_1d (grid1d.hpp:66-69), on the device; the
+// element matrices are those of the table's order.
+inline GridFunction1D apply_mass_1d(const GridFunction1D& v, const SpectralTable& table) {
+  require(v.order == table.order, "apply_mass_1d: order mismatch");
+  std::vector<double> x = v.to_dof(), y(x.size());
+  check(sfem_cuda_lines_host(table.handle(), SFEM_OP_APPLY_MASS, 1, x.data(), y.data()));
+  return GridFunction1D::from_dof(y.data(), v.order, v.elements);
+}
+inline GridFunction1D apply_stiffness_1d(const GridFunction1D& v, const SpectralTable& table) {
+  require(v.order == table.order, "apply_stiffness_1d: order mismatch");
+  std::vector<double> x = v.to_dof(), y(x.size());
+  check(sfem_cuda_lines_host(table.handle(), SFEM_OP_APPLY_STIFFNESS, 1, x.data(), y.data()));
+  return GridFunction1D::from_dof(y.data(), v.order, v.elements);
+}
+
+// materialize_eigenvector (spectral.hpp:330)
+inline GridFunction1D materialize_eigenvector(const SpectralTable& table, int k, int l) {
+  std::vector<double> y(table.coeff_count());
+  check(sfem_cuda_table_eigenvector(table.handle(), k, l, y.data()));
+  return GridFunction1D::from_dof(y.data(), table.order, table.elements);
+}
+
+// DirectRoute (eigenbasis.hpp:28): Spectral runs F_n, MassApply the mass
+// operator followed by FC_n (the reference's cross-check route).
+enum class DirectRoute { Spectral, MassApply };
+
+inline CoefficientArray1D decompose(const GridFunction1D& w, const SpectralTable& table,
+                                    DirectRoute route = DirectRoute::Spectral) {
   require(w.order == table.order && w.elements == table.elements,
           "decompose: grid function does not match the table");
+  if (route == DirectRoute::MassApply) return decompose_weighted(apply_mass_1d(w, table), table);
   CoefficientArray1D c = CoefficientArray1D::zeros(table.order, table.elements);
   const std::vector<double> v = w.to_dof();
   lines::decompose(table, v.data(), c.data.data());

@@ -93,10 +93,22 @@ int sfem_cuda_table_file_read(const char* path, int order, int elements, double*
  * for the analyses, coefficient layout for synthesis).  In-place allowed when
  * in == out and the pitches agree. */
 enum { SFEM_OP_DECOMPOSE_WEIGHTED = 0, SFEM_OP_DECOMPOSE = 1, SFEM_OP_SYNTHESIZE = 2 };
+/* Element stencils on the same dof-layout lines (grid1d.cpp:7-47):
+ *   SFEM_OP_APPLY_MASS       apply_mass_1d       y = M v
+ *   SFEM_OP_APPLY_STIFFNESS  apply_stiffness_1d  y = A v
+ * with the reference-element matrices of the table's order (no h scaling, as
+ * the reference).  Boundary nodes are absent from the dof layout.  Together
+ * with SFEM_OP_DECOMPOSE_WEIGHTED, APPLY_MASS gives decompose's
+ * DirectRoute::MassApply (eigenbasis.cpp:469-470). */
+enum { SFEM_OP_APPLY_MASS = 3, SFEM_OP_APPLY_STIFFNESS = 4 };
 int sfem_cuda_lines_device(sfem_table table, int op, long long count, const double* d_in,
                            long long in_pitch, double* d_out, long long out_pitch, void* stream);
 /* Same on host buffers (dense, pitch = L); host<->device copies included. */
 int sfem_cuda_lines_host(sfem_table table, int op, long long count, const double* h_in, double* h_out);
+/* materialize_eigenvector (spectral.hpp:330, spectral.cpp:238-265): the grid
+ * values of eigenvector (k, l) (k = 0: l = 1..n-1; k >= 1: l = 1..n) in the
+ * dof layout (n*K-1 doubles, host memory), from the table's primaries. */
+int sfem_cuda_table_eigenvector(sfem_table table, int k, int l, double* out);
 
 /* Solve plan for  -sum_i a_i d^2u/dx_i^2 + shift*u = f  on the box
  * prod [0, lengths_i] with homogeneous Dirichlet data, orders n_i and K_i

@@ -27,6 +27,7 @@
 #include "sfem/banded.hpp"
 #include "sfem/cases.hpp"
 #include "sfem/eigenbasis.hpp"
+#include "sfem/grid1d.hpp"
 #include "sfem/poisson.hpp"
 #include "sfem/spectral.hpp"
 #include "sfem/trig.hpp"
@@ -225,6 +226,29 @@ int sfemref_tableset_get(const char* dir, int write_cache, int n, int K, double*
     TableSet ts(Precision::Double, dir, write_cache != 0);
     export_table(ts.get(n, K), theta, half_cos, half_sin, values, norm_sq, nodal_weight, p, q, interior_values,
                  interior_vectors, eig_coeff);
+  });
+}
+
+// apply_mass_1d (kind 0) / apply_stiffness_1d (kind 1) (grid1d.cpp:33-47) on
+// `count` dof-layout lines.
+int sfemref_apply_1d(int kind, int n, int K, long long count, const double* in, double* out) {
+  return guarded([&] {
+    const SpectralTable1D& t = tables().get(n, K);
+    const int L = n * K - 1;
+    for (long long b = 0; b < count; ++b) {
+      GridFunction1D g = GridFunction1D::zeros(n, K);
+      scatter_dof_line(n, K, in + b * L, g.nodal.data(), 1, g.interior.data(), 1);
+      const GridFunction1D y = kind == 0 ? apply_mass_1d(g, t.element) : apply_stiffness_1d(g, t.element);
+      gather_dof_line(n, K, y.nodal.data(), 1, y.interior.data(), 1, out + b * L);
+    }
+  });
+}
+
+// materialize_eigenvector (spectral.cpp:238-265), dof layout.
+int sfemref_eigenvector(int n, int K, int k, int l, double* out) {
+  return guarded([&] {
+    const GridFunction1D g = materialize_eigenvector(tables().get(n, K), k, l);
+    gather_dof_line(n, K, g.nodal.data(), 1, g.interior.data(), 1, out);
   });
 }
 

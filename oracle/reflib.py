@@ -35,6 +35,8 @@ def lib():
         L.sfemref_save_table.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
         L.sfemref_load_table.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int] + [_dp] * 11
         L.sfemref_tableset_get.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int] + [_dp] * 11
+        L.sfemref_apply_1d.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, _dp, _dp]
+        L.sfemref_eigenvector.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
         L.sfemref_element.argtypes = [ctypes.c_int, _dp, _dp]
         L.sfemref_lines.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, _dp, _dp]
         L.sfemref_solve.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
@@ -113,6 +115,21 @@ def load_table(path: str, n: int, K: int) -> dict:
 def tableset_get(cache_dir: str, write_cache: bool, n: int, K: int) -> dict:
     """TableSet(Double, cache_dir, write_cache).get(n, K) (poisson.cpp:49-73)."""
     return _table_export(n, K, lambda *a: lib().sfemref_tableset_get(cache_dir.encode(), int(write_cache), n, K, *a))
+
+
+def apply_1d(kind: str, n: int, K: int, x: np.ndarray) -> np.ndarray:
+    """apply_mass_1d / apply_stiffness_1d (grid1d.cpp:33-47) of dof-layout lines."""
+    x = np.ascontiguousarray(np.atleast_2d(x), float)
+    y = np.empty_like(x)
+    _chk(lib().sfemref_apply_1d({"mass": 0, "stiffness": 1}[kind], n, K, x.shape[0], _p(x), _p(y)))
+    return y
+
+
+def eigenvector(n: int, K: int, k: int, l: int) -> np.ndarray:
+    """materialize_eigenvector (spectral.cpp:238-265), dof layout."""
+    y = np.empty(n * K - 1)
+    _chk(lib().sfemref_eigenvector(n, K, k, l, _p(y)))
+    return y
 
 
 def element(n: int):

@@ -29,7 +29,8 @@ __all__ = [
     "solve_dof", "synthesize", "decompose", "decompose_weighted", "lines", "lines_device", "DECOMPOSE_WEIGHTED",
     "DECOMPOSE", "SYNTHESIZE", "default_context", "HEADER_SYMBOLS", "Field", "solve", "FIELD_CONSTANT",
     "FIELD_SINES", "FIELD_SIN1D", "FIELD_POISSON2D", "FIELD_POISSON3D", "CASE_FIELDS", "TABLE_TEXT",
-    "TABLE_BINARY", "build_and_save_table", "read_table_file",
+    "TABLE_BINARY", "build_and_save_table", "read_table_file", "APPLY_MASS", "APPLY_STIFFNESS", "DirectRoute",
+    "apply_mass_1d", "apply_stiffness_1d", "materialize_eigenvector",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -38,6 +39,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.environ.get("SFEM_LIB") or os.path.join(_HERE, "libsfem_b200.so")
 
 DECOMPOSE_WEIGHTED, DECOMPOSE, SYNTHESIZE = 0, 1, 2
+APPLY_MASS, APPLY_STIFFNESS = 3, 4  # element stencils (grid1d.cpp:7-47)
+
+
+class DirectRoute:
+    """Route of decompose (eigenbasis.hpp:28): SPECTRAL runs F_n directly, MASS_APPLY applies the
+    mass operator and then FC_n (the reference's cross-check route)."""
+    SPECTRAL = 0
+    MASS_APPLY = 1
 # built-in right-hand sides of sfem_cuda_fem_load (include/sfem_cuda.h)
 FIELD_CONSTANT, FIELD_SINES, FIELD_SIN1D, FIELD_POISSON2D, FIELD_POISSON3D = 0, 1, 2, 3, 4
 # the reference's manufactured case names (cases.hpp:20) -> field
@@ -83,6 +92,7 @@ _SIGS = [
     ("sfem_cuda_lines_device", ctypes.c_int,
      [_vp, ctypes.c_int, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp]),
     ("sfem_cuda_lines_host", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_longlong, _dp, _dp]),
+    ("sfem_cuda_table_eigenvector", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _dp]),
     ("sfem_cuda_plan_create", ctypes.c_int,
      [_vp, ctypes.c_int, _ip, _ip, _dp, _dp, ctypes.c_double, ctypes.POINTER(_vp)]),
     ("sfem_cuda_plan_destroy", ctypes.c_int, [_vp]),
@@ -368,11 +378,34 @@ def decompose_weighted(y: GridFunction1D, table: SpectralTable) -> CoefficientAr
     return CoefficientArray1D(table.order, table.elements, lines(table, DECOMPOSE_WEIGHTED, y.to_dof())[0])
 
 
-def decompose(w: GridFunction1D, table: SpectralTable) -> CoefficientArray1D:
-    """eigenbasis.cpp:466-475 (Spectral route)."""
+def decompose(w: GridFunction1D, table: SpectralTable, route: int = DirectRoute.SPECTRAL) -> CoefficientArray1D:
+    """eigenbasis.cpp:466-475."""
     if w.order != table.order or w.elements != table.elements:
         raise Error("decompose: grid function does not match the table")
+    if route == DirectRoute.MASS_APPLY:
+        return decompose_weighted(apply_mass_1d(w, table), table)
     return CoefficientArray1D(table.order, table.elements, lines(table, DECOMPOSE, w.to_dof())[0])
+
+
+def apply_mass_1d(v: GridFunction1D, table: SpectralTable) -> GridFunction1D:
+    """apply_mass_1d (grid1d.cpp:33-39), on the device; the element matrices are the table's."""
+    if v.order != table.order:
+        raise Error("apply_mass_1d: order mismatch")
+    return GridFunction1D.from_dof(lines(table, APPLY_MASS, v.to_dof())[0], v.order, v.elements)
+
+
+def apply_stiffness_1d(v: GridFunction1D, table: SpectralTable) -> GridFunction1D:
+    """apply_stiffness_1d (grid1d.cpp:41-47), on the device."""
+    if v.order != table.order:
+        raise Error("apply_stiffness_1d: order mismatch")
+    return GridFunction1D.from_dof(lines(table, APPLY_STIFFNESS, v.to_dof())[0], v.order, v.elements)
+
+
+def materialize_eigenvector(table: SpectralTable, k: int, l: int) -> GridFunction1D:
+    """materialize_eigenvector (spectral.cpp:238-265): grid values of eigenvector (k, l)."""
+    out = np.empty(table.coeff_count)
+    _check(lib.sfem_cuda_table_eigenvector(table.handle, k, l, _dptr(out)))
+    return GridFunction1D.from_dof(out, table.order, table.elements)
 
 
 # ---------------------------------------------------------------------------

@@ -1170,6 +1170,35 @@ int sfem_cuda_table_file_read(const char* path, int order, int elements, double*
   });
 }
 
+int sfem_cuda_table_eigenvector(sfem_table t, int k, int l, double* out) {
+  return guarded([&] {
+    require(t && out, "materialize_eigenvector: null argument");
+    const HostTable& h = t->host;
+    const int n = h.order, K = h.elements, m = n - 1;
+    require(k >= 0 && k < K, "materialize_eigenvector: frequency out of range");
+    require(l >= 1 && l <= (k == 0 ? m : n), "materialize_eigenvector: branch out of range");
+    // spectral.cpp:238-265, written in the dof layout (node j at j*n - 1,
+    // interior i of element j-1 at (j-1)*n + i)
+    const double pi = M_PI;
+    std::fill(out, out + (static_cast<size_t>(n) * K - 1), 0.0);
+    if (k == 0) {
+      for (int j = 1; j <= K; ++j)
+        for (int i = 0; i < m; ++i)
+          out[static_cast<size_t>(j - 1) * n + i] =
+              (j % 2 == 1) ? h.interior_vectors[static_cast<size_t>(i) * m + (l - 1)]
+                           : -h.interior_vectors[static_cast<size_t>(m - 1 - i) * m + (l - 1)];
+      return;
+    }
+    for (int j = 1; j < K; ++j) out[static_cast<size_t>(j) * n - 1] = std::sin(pi * k * j / static_cast<double>(K));
+    const double* p = h.p.data() + (static_cast<size_t>(k - 1) * n + (l - 1)) * m;
+    for (int j = 1; j <= K; ++j) {
+      const double s_left = std::sin(pi * k * (j - 1) / static_cast<double>(K));
+      const double s_right = std::sin(pi * k * j / static_cast<double>(K));
+      for (int i = 0; i < m; ++i) out[static_cast<size_t>(j - 1) * n + i] = p[i] * s_left + p[m - 1 - i] * s_right;
+    }
+  });
+}
+
 int sfem_cuda_table_destroy(sfem_table t) {
   return guarded([&] {
     if (!t) return;
@@ -1198,7 +1227,7 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
                            double* d_out, long long out_pitch, void* stream) {
   return guarded([&] {
     require(t != nullptr, "lines: null table");
-    require(op >= 0 && op <= 2, "lines: unknown op");
+    require(op >= 0 && op <= SFEM_OP_APPLY_STIFFNESS, "lines: unknown op");
     require(count >= 0, "lines: negative count");
     const long long L = t->dev.L;
     require(in_pitch >= L && out_pitch >= L, "lines: pitch smaller than the line length");
@@ -1211,6 +1240,29 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
                            count, cudaMemcpyDeviceToDevice, s),
          "lines: repitch");
       src = d_out;
+    }
+    if (op == SFEM_OP_APPLY_MASS || op == SFEM_OP_APPLY_STIFFNESS) {
+      // apply_mass_1d / apply_stiffness_1d (grid1d.cpp:33-47): the element
+      // stencil as one operator sweep along the rows, y = shift M v + fac S v
+      // with (shift, fac) = (1, 0) or (0, 1) (fem_ops.cu op_rows; in place).
+      OpAxisArgs a{};
+      const int np = t->dev.n + 1;
+      a.n = t->dev.n;
+      a.K = t->dev.K;
+      a.L = L;
+      a.outer = count;
+      a.inner = 1;
+      a.pitch = out_pitch;
+      a.last = L;
+      a.shift = op == SFEM_OP_APPLY_MASS ? 1.0 : 0.0;
+      a.fac = op == SFEM_OP_APPLY_MASS ? 0.0 : 1.0;
+      for (int r = 0; r < np; ++r)
+        for (int c = 0; c < np; ++c) {
+          a.M[r][c] = t->host.mass[static_cast<size_t>(r) * np + c];
+          a.S[r][c] = t->host.stiffness[static_cast<size_t>(r) * np + c];
+        }
+      ck(launch_op_axis(src, nullptr, d_out, nullptr, a, true, true, true, false, nullptr, s), "lines: element stencil");
+      return;
     }
     LineSet ls{};
     ls.src = src;

@@ -174,10 +174,13 @@ __device__ __forceinline__ void fft_pass(double2* W, const double2* __restrict__
   __syncthreads();
 }
 
+#ifndef SFEM_MID_DIAG_SKIP
+#define SFEM_MID_DIAG_SKIP 0  // diagnostics builds only: 1 skips the FFT passes, 2 the mixes
+#endif
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
   using PL = Plan<C::N, (C::J <= 8)>;
-  if constexpr (P < PL::NP) {
+  if constexpr (P < PL::NP && SFEM_MID_DIAG_SKIP != 1) {
     constexpr int R = PL::R[P];
     fft_pass<C, R, NS>(W, tw);
     fft<C, P + 1, NS * R>(W, tw);
@@ -437,7 +440,7 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 #else
 #define MIDX(a, b) ((a) * n + (b))
 #endif
-  constexpr int ITEMS = (N - 1) * B + B;
+  constexpr int ITEMS = (SFEM_MID_DIAG_SKIP == 2) ? 0 : (N - 1) * B + B;
   for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
     if (it < (N - 1) * B) {
       const int k = 1 + it / B, b = it % B;
@@ -663,7 +666,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool o
 }
 
 template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
-__global__ void __launch_bounds__(TH, TH == 512 ? 1 : 2)  // 256-thread tiles: two CTAs per SM
+__global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 registers
     sweep_mid(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
               const double* __restrict__ e0F) {
   using C = Cfg<NN, K, BB, TH, ROWS>;
@@ -910,14 +913,31 @@ SFEM_PHASE_EXPORT(sfem_debug_phase_records_mid)
 
 }  // namespace mid
 
-#ifndef SFEM_MID_N1_B4
-#define SFEM_MID_N1_B4 0
+// Lines per tile and threads per CTA of the C5 shapes.
+#ifndef SFEM_MID_B_N1
+#define SFEM_MID_B_N1 8
 #endif
-// Threads per CTA for the B = 8 tiles that fit two CTAs per SM.
-#ifndef SFEM_MID_TH256
-#define SFEM_MID_TH256 1
+#ifndef SFEM_MID_TH_N1
+#define SFEM_MID_TH_N1 512
 #endif
-constexpr int kMidTH = SFEM_MID_TH256 ? 256 : 512;
+#ifndef SFEM_MID_B_N2
+#define SFEM_MID_B_N2 8
+#endif
+#ifndef SFEM_MID_TH_N2
+#define SFEM_MID_TH_N2 256
+#endif
+#ifndef SFEM_MID_B_N4
+#define SFEM_MID_B_N4 8
+#endif
+#ifndef SFEM_MID_TH_N4
+#define SFEM_MID_TH_N4 256
+#endif
+#ifndef SFEM_MID_B_N9
+#define SFEM_MID_B_N9 8
+#endif
+#ifndef SFEM_MID_TH_N9
+#define SFEM_MID_TH_N9 256
+#endif
 
 bool has_mid_sweep(int n, int K) {
   return (n == 1 && K == 1024) || (n == 2 && K == 512) || (n == 4 && K == 256) || (n == 9 && K == 114) ||
@@ -938,14 +958,15 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int
     if (!gwork) return cudaErrorInvalidValue;
     return mid::launch_gw<4, 4096, 1, 512>(t, ls, mode, analysis, sym, gwork, stream);
   }
-#if SFEM_MID_N1_B4
-  if (t.n == 1 && t.K == 1024) return mid::launch<1, 1024, 4, 256>(t, ls, mode, analysis, sym, stream);
-#else
-  if (t.n == 1 && t.K == 1024) return mid::launch<1, 1024, 8, 512>(t, ls, mode, analysis, sym, stream);
-#endif
-  if (t.n == 2 && t.K == 512) return mid::launch<2, 512, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
-  if (t.n == 4 && t.K == 256) return mid::launch<4, 256, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
-  if (t.n == 9 && t.K == 114) return mid::launch<9, 114, 8, kMidTH>(t, ls, mode, analysis, sym, stream);
+  // (lines per tile, threads) per shape
+  if (t.n == 1 && t.K == 1024)
+    return mid::launch<1, 1024, SFEM_MID_B_N1, SFEM_MID_TH_N1>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 2 && t.K == 512)
+    return mid::launch<2, 512, SFEM_MID_B_N2, SFEM_MID_TH_N2>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 4 && t.K == 256)
+    return mid::launch<4, 256, SFEM_MID_B_N4, SFEM_MID_TH_N4>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 9 && t.K == 114)
+    return mid::launch<9, 114, SFEM_MID_B_N9, SFEM_MID_TH_N9>(t, ls, mode, analysis, sym, stream);
   if (t.n == 9 && t.K == 1024) return mid::launch<9, 1024, 2, 512>(t, ls, mode, analysis, sym, stream);
   return cudaErrorNotSupported;
 }

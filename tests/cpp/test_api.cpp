@@ -329,9 +329,31 @@ static void table_files() {
   std::system(("rm -rf " + dir).c_str());
 }
 
+// test_eigenbasis.cpp:40-50, 125-135: synthesize(indicator (k, l)) is the
+// materialised eigenvector; both DirectRoutes give the same coefficients.
+static void eigenvectors_and_routes(TableSet& tables) {
+  for (int n : {1, 3, 9})
+    for (int K : {4, 11}) {
+      const auto& t = tables.get(n, K);
+      for (int k = 0; k < K; ++k)
+        for (int l = 1; l <= (k == 0 ? n - 1 : n); ++l) {
+          CoefficientArray1D c = CoefficientArray1D::zeros(n, K);
+          c.at(k, l) = 1.0;
+          const GridFunction1D s = synthesize(c, t), want = materialize_eigenvector(t, k, l);
+          CHECK(max_diff(s.to_dof(), want.to_dof()) <= 1e-12);
+        }
+      const GridFunction1D g = random_grid(n, K, 5);
+      const auto a = decompose(g, t, DirectRoute::Spectral), b = decompose(g, t, DirectRoute::MassApply);
+      CHECK(max_diff(a.data, b.data) <= 1e-12);
+    }
+  CHECK_THROWS(materialize_eigenvector(tables.get(3, 4), 4, 1));
+  CHECK_THROWS(materialize_eigenvector(tables.get(3, 4), 0, 3));
+}
+
 int main() {
   TableSet tables;
   table_files();
+  eigenvectors_and_routes(tables);
   roundtrip_identities(tables);
   dimension_mismatches(tables);
   solve_vs_dense(tables);
