@@ -103,19 +103,48 @@ struct Plan<114, FEW> {
 
 __device__ __forceinline__ int makhoul_src(int t, int N) { return (2 * t < N) ? 2 * t : 2 * N - 1 - 2 * t; }
 
-// Direct DFT of odd length R with roots from the K-point twiddle table.
+// Direct DFT of odd length R (K = 114: R = 19) with roots from the K-point
+// twiddle table, by conjugate pairs: with s_q = x_q + x_{R-q}, d_q = x_q -
+// x_{R-q} and theta = 2 pi q p / R,
+//   y_p     = x_0 + sum_q s_q cos(theta) - i sum_q d_q sin(theta)
+//   y_{R-p} = x_0 + sum_q s_q cos(theta) + i sum_q d_q sin(theta),
+// so an output pair costs 4 (R-1)/2 real FMAs and the (R-1)/2 roots are
+// loaded once per butterfly (was R-1 complex products and loads per output).
 template <int R, int K>
 __device__ __forceinline__ void dft_direct(double2 (&x)[R], const double2* __restrict__ tw) {
-  double2 y[R];
+  constexpr int H = (R - 1) / 2;
+  double cs[H + 1], sn[H + 1];  // cos / sin (2 pi j / R), j = 1..H
 #pragma unroll
-  for (int p = 0; p < R; ++p) {
-    double2 s = x[0];
+  for (int j = 1; j <= H; ++j) {
+    const double2 w = __ldg(tw + j * (K / R));  // exp(-2 pi i j / R)
+    cs[j] = w.x;
+    sn[j] = -w.y;
+  }
+  double2 sq[H + 1], dq[H + 1];
+  double2 y0 = x[0];
 #pragma unroll
-    for (int q = 1; q < R; ++q) s = c_add(s, c_mul(x[q], __ldg(tw + ((q * p) % R) * (K / R))));
-    y[p] = s;
+  for (int q = 1; q <= H; ++q) {
+    sq[q] = c_add(x[q], x[R - q]);
+    dq[q] = c_sub(x[q], x[R - q]);
+    y0 = c_add(y0, sq[q]);
   }
 #pragma unroll
-  for (int p = 0; p < R; ++p) x[p] = y[p];
+  for (int p = 1; p <= H; ++p) {
+    double2 a = x[0], b = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 1; q <= H; ++q) {
+      const int j = (q * p) % R;
+      const double c = j <= H ? cs[j] : cs[R - j];
+      const double sv = j <= H ? sn[j] : -sn[R - j];
+      a.x = fma(sq[q].x, c, a.x);
+      a.y = fma(sq[q].y, c, a.y);
+      b.x = fma(dq[q].x, sv, b.x);
+      b.y = fma(dq[q].y, sv, b.y);
+    }
+    x[p] = make_double2(a.x + b.y, a.y - b.x);
+    x[R - p] = make_double2(a.x - b.y, a.y + b.x);
+  }
+  x[0] = y0;
 }
 
 template <int R, int K>
