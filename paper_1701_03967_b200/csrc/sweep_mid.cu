@@ -446,6 +446,25 @@ __device__ __forceinline__ void forward_post(const double2* Z, double* R, const 
 }
 
 // ------------------------------------------------------------ mixes
+// Symbol divide c / d (d > 0): MUFU reciprocal seed, one Newton step, one
+// residual correction of the quotient -- within 1 ulp of IEEE division (the
+// fast kernels' sym_div, measured over 2^30 quotients by tools/div_ulp.cu)
+// at a third of the instructions of the IEEE division sequence.
+#ifndef SFEM_MID_FAST_DIV
+#define SFEM_MID_FAST_DIV 1
+#endif
+__device__ __forceinline__ double mid_div(double c, double d) {
+#if SFEM_MID_FAST_DIV
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  const double q = c * r;
+  return fma(fma(-d, q, c), r, q);
+#else
+  return c / d;
+#endif
+}
+
 // Per (k >= 1, line) item, in place at tile positions m + (k-1) n + [0, n):
 //   MODE kForward:             c = Mf v
 //   MODE kInverse:             u = Mi c
@@ -490,7 +509,7 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
           double acc = 0.0;
 #pragma unroll
           for (int s = 0; s < n; ++s) acc = fma(__ldg(M + MIDX(l, s)), v[s], acc);
-          if (MODE == kForwardDivideInverse) acc = acc / (base[b] + f_last * __ldg(eig + m + (k - 1) * n + l));
+          if (MODE == kForwardDivideInverse) acc = mid_div(acc, base[b] + f_last * __ldg(eig + m + (k - 1) * n + l));
           c[l] = acc;
         }
       } else {
@@ -529,7 +548,7 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
           double acc = 0.0;
 #pragma unroll
           for (int i = 0; i < m; ++i) acc = fma(C0[i * B + b], __ldg(e0F + i * m + l), acc);
-          if (MODE == kForwardDivideInverse) acc = acc / (base[b] + f_last * __ldg(eig + l));
+          if (MODE == kForwardDivideInverse) acc = mid_div(acc, base[b] + f_last * __ldg(eig + l));
           c[l] = acc;
         }
       } else {
