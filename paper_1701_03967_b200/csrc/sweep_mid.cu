@@ -713,6 +713,25 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool o
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+// Strided tiles whose B lines are adjacent, 16-byte aligned and all present:
+// each position row (B doubles, contiguous in both places) moves as B/2
+// 16-byte copies / stores instead of B 8-byte ones.
+template <class C>
+__device__ __forceinline__ bool vec_tile(const long long* off, int Bv, long long ps, const double* src,
+                                         const double* dst) {
+  if constexpr (C::ROWS || (C::B & 1)) return false;
+  bool ok = Bv == C::B && (off[0] & 1) == 0 && (ps & 1) == 0 &&
+            ((reinterpret_cast<unsigned long long>(src) | reinterpret_cast<unsigned long long>(dst)) & 15) == 0;
+#pragma unroll
+  for (int b = 1; b < C::B; ++b) ok = ok && off[b] == off[0] + b;
+  return ok;
+}
+
 template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
 __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 registers
     sweep_mid(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
@@ -759,10 +778,18 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
 
   // tile load, all copies in flight at once (phantom lines zero-filled)
   const long long ps = ls.ps;
+  const bool vec = vec_tile<C>(off, Bv, ps, ls.src, ls.dst);
   if (ROWS) {
     for (int it = threadIdx.x; it < L * B; it += TH) {
       const int b = it / L, pos = it - b * L;
       cp_async8(R + C::ix(pos, b), ls.src + off[b] + pos, b < Bv);
+    }
+  } else if (vec) {
+    constexpr int B2 = B / 2;
+    const double* src = ls.src + off[0];
+    for (int it = threadIdx.x; it < L * B2; it += TH) {
+      const int pos = it / B2, b2 = it - pos * B2;
+      cp_async16(R + 2 * it, src + pos * ps + 2 * b2);
     }
   } else {
     for (int it = threadIdx.x; it < L * B; it += TH) {
@@ -794,6 +821,13 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
     for (int it = threadIdx.x; it < L * B; it += TH) {
       const int b = it / L, pos = it - b * L;
       if (b < Bv) ls.dst[off[b] + pos] = R[C::ix(pos, b)];
+    }
+  } else if (vec) {
+    constexpr int B2 = B / 2;
+    double* dst = ls.dst + off[0];
+    for (int it = threadIdx.x; it < L * B2; it += TH) {
+      const int pos = it / B2, b2 = it - pos * B2;
+      *reinterpret_cast<double2*>(dst + pos * ps + 2 * b2) = *reinterpret_cast<const double2*>(R + 2 * it);
     }
   } else {
     for (int it = threadIdx.x; it < L * B; it += TH) {
