@@ -27,6 +27,14 @@
 #ifndef SFEM_MID_R16
 #define SFEM_MID_R16 1
 #endif
+// CTAs of at least this many threads hold one radix-16 item per thread, so
+// they take the short radix plans regardless of the job count.
+#ifndef SFEM_MID_FEW_TH
+#define SFEM_MID_FEW_TH 512
+#endif
+#ifndef SFEM_MID_C3_TH
+#define SFEM_MID_C3_TH 512
+#endif
 #ifndef SFEM_MID_KMIX
 #define SFEM_MID_KMIX 1
 #endif
@@ -208,7 +216,7 @@ __device__ __forceinline__ void fft_pass(double2* W, const double2* __restrict__
 #endif
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
-  using PL = Plan<C::N, (C::J <= 8)>;
+  using PL = Plan<C::N, (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH)>;
   if constexpr (P < PL::NP && SFEM_MID_DIAG_SKIP != 1) {
     constexpr int R = PL::R[P];
     fft_pass<C, R, NS>(W, tw);
@@ -264,7 +272,7 @@ __device__ __forceinline__ void fft_pass_oop(const double2* X, double2* Y, const
 // Returns the buffer holding the result.
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ double2* fft_oop(double2* X, double2* Y, const double2* __restrict__ tw) {
-  using PL = Plan<C::N, (C::J <= 8)>;
+  using PL = Plan<C::N, (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH)>;
   if constexpr (P < PL::NP) {
     constexpr int R = PL::R[P];
     fft_pass_oop<C, R, NS>(X, Y, tw);
@@ -1049,7 +1057,7 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int
     return mid::launch<4, 256, SFEM_MID_B_N4, SFEM_MID_TH_N4>(t, ls, mode, analysis, sym, stream);
   if (t.n == 9 && t.K == 114)
     return mid::launch<9, 114, SFEM_MID_B_N9, SFEM_MID_TH_N9>(t, ls, mode, analysis, sym, stream);
-  if (t.n == 9 && t.K == 1024) return mid::launch<9, 1024, 2, 512>(t, ls, mode, analysis, sym, stream);
+  if (t.n == 9 && t.K == 1024) return mid::launch<9, 1024, 2, SFEM_MID_C3_TH>(t, ls, mode, analysis, sym, stream);
   return cudaErrorNotSupported;
 }
 
