@@ -32,6 +32,9 @@
 #ifndef SFEM_MID_FEW_TH
 #define SFEM_MID_FEW_TH 512
 #endif
+#ifndef SFEM_MID_C2_TH
+#define SFEM_MID_C2_TH 512
+#endif
 #ifndef SFEM_MID_C3_TH
 #define SFEM_MID_C3_TH 512
 #endif
@@ -1046,7 +1049,7 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int
   if (ls.nlines <= 0) return cudaSuccess;
   if (t.n == 4 && t.K == 4096) {
     if (!gwork) return cudaErrorInvalidValue;
-    return mid::launch_gw<4, 4096, 1, 512>(t, ls, mode, analysis, sym, gwork, stream);
+    return mid::launch_gw<4, 4096, 1, SFEM_MID_C2_TH>(t, ls, mode, analysis, sym, gwork, stream);
   }
   // (lines per tile, threads) per shape
   if (t.n == 1 && t.K == 1024)
