@@ -832,7 +832,6 @@ HostTable parse_binary(const std::string& s, const std::string& path, int n, int
   if (s.size() < sizeof h) fail("load_table: malformed header in '" + path + "'");
   std::memcpy(&h, s.data(), sizeof h);
   check_header(h.order, h.elements, n, K);
-  const int m = n - 1;
   HostTable t = table_skeleton(build_element(n), K);
   size_t count = 0;
   for (auto* v : binary_parts(t)) count += v->size();
@@ -846,7 +845,6 @@ HostTable parse_binary(const std::string& s, const std::string& path, int n, int
     std::memcpy(v->data(), p, v->size() * sizeof(double));
     p += v->size() * sizeof(double);
   }
-  (void)m;
   return t;
 }
 
