@@ -1,0 +1,1095 @@
+// Sweep kernels for mid-length lines (templates; instantiated by sweep_mid.cu
+// for the tuned shapes and by sweep_mid_k*.cu for the general ones) (n*K ~ 1000-10000): C5's (n, K) in
+// {(1,1024), (2,512), (4,256), (9,114)} and C3's (9,1024).
+//
+// Same mathematics as sweep.cu (reference eigenbasis.cpp:63-225),
+// specialised at compile time on (n, K, lines per tile B, threads) and laid
+// out for one large tile per CTA:
+//   * one shared-memory region is reused in place for every stage: the tile
+//     T[pos][b], the FFT buffer W[t][job] (complex) and the per-frequency slots
+//     S, which are stored at the tile positions of the coefficients they
+//     become (S row r <-> tile position m + r).  Stages that permute data move
+//     it through registers ("bridges": every thread loads its items, barrier,
+//     every thread stores);
+//   * FFTs are in-place Stockham passes with compile-time radices (16/8/4/2
+//     register butterflies, odd radices 3 and 19 as direct DFTs);
+//   * the n x n mix of a frequency touches only that frequency's n slots of a
+//     line, so it runs in place per (k, line) item; the last-axis kernel does
+//     forward mix, symbol divide and inverse mix of an item in registers;
+//   * the zero-frequency centre sums (eigenbasis.cpp:31-40) are chunked over
+//     all threads and reduced in a fixed order (deterministic).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "fft_reg.cuh"
+#include "sweep.cuh"
+
+#ifndef SFEM_MID_R16
+#define SFEM_MID_R16 1
+#endif
+// CTAs of at least this many threads hold one radix-16 item per thread, so
+// they take the short radix plans regardless of the job count.
+#ifndef SFEM_MID_FEW_TH
+#define SFEM_MID_FEW_TH 512
+#endif
+#ifndef SFEM_MID_C2_TH
+#define SFEM_MID_C2_TH 512
+#endif
+#ifndef SFEM_MID_C3_TH
+#define SFEM_MID_C3_TH 512
+#endif
+#ifndef SFEM_MID_KMIX
+#define SFEM_MID_KMIX 1
+#endif
+
+namespace sfem_b200 {
+namespace mid {
+
+using namespace reg;
+
+#include "phase_timing.cuh"
+
+// ROWS: tile stored line-major T[b][pos] (line pitch LP, odd: conflict-free
+// for lanes over lines), used when lines are rows of the tensor; otherwise
+// position-major T[pos][b] (strided axes, lanes over the 8 adjacent lines).
+template <int NN, int K, int BB, int TH, bool ROWS_, bool GW = false>
+struct Cfg {
+  static constexpr int n = NN, m = NN - 1, half = m / 2, ne = NN / 2, N = K, L = NN * K - 1;
+  static constexpr bool ROWS = ROWS_;
+  static constexpr int LP = L | 1;
+  static constexpr int PSTR = ROWS ? 1 : BB;  // position stride in the tile
+  __device__ __forceinline__ static constexpr int ix(int pos, int b) { return ROWS ? b * LP + pos : pos * BB + b; }
+  static constexpr int B = BB, Bh = (BB + 1) / 2, Bm = (m & 1) ? Bh : 0;
+  static constexpr int NPAIR = B * half;
+  static constexpr int J = NPAIR + Bm + 2 * Bh;
+  static constexpr int THREADS = TH;
+  static constexpr int WD = 2 * J * K;  // FFT buffer (doubles)
+  static constexpr int TD = (ROWS ? LP : L) * B;  // tile (doubles)
+  static constexpr int REGION = (GW || TD > WD) ? TD : WD;  // GW: FFT work in global scratch
+  static constexpr int NCEN = m * B;  // centre sums
+  static constexpr int CHUNKS = NCEN > 0 ? (TH / NCEN > 0 ? TH / NCEN : 1) : 1;
+  static constexpr int ECH = (K + CHUNKS - 1) / CHUNKS;  // elements per chunk
+  static constexpr int C0_OFF = REGION;
+  static constexpr int PS_OFF = C0_OFF + (NCEN > 0 ? NCEN : 1);
+  static constexpr int BASE_OFF = PS_OFF + (NCEN > 0 ? CHUNKS * NCEN : 1);
+  static constexpr int TOTAL = BASE_OFF + B;
+  static constexpr size_t SMEM = static_cast<size_t>(TOTAL) * sizeof(double);
+};
+
+// Radix plans (product = K), chosen so that one pass keeps at most ~24
+// complex values per thread in flight (FEW: at most 8 jobs per tile, where
+// a radix-16 pass still fits).
+template <int K, bool FEW>
+struct Plan;
+template <bool FEW>
+struct Plan<1024, FEW> {
+#if SFEM_MID_R16
+  static constexpr int NP = FEW ? 3 : 4;
+  static constexpr int R[4] = {FEW ? 16 : 8, 8, FEW ? 8 : 4, 4};
+#else
+  static constexpr int NP = 4;
+  static constexpr int R[4] = {8, 8, 4, 4};
+#endif
+};
+template <bool FEW>
+struct Plan<512, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 8, 8};
+};
+template <bool FEW>
+struct Plan<256, FEW> {
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {16, 16};
+};
+template <bool FEW>
+struct Plan<128, FEW> {
+  static constexpr int NP = FEW ? 2 : 3;
+  static constexpr int R[3] = {FEW ? 16 : 8, FEW ? 8 : 4, 4};
+};
+template <bool FEW>
+struct Plan<64, FEW> {
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {8, 8};
+};
+template <bool FEW>
+struct Plan<32, FEW> {
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {8, 4};
+};
+template <bool FEW>
+struct Plan<16, FEW> {
+  static constexpr int NP = 1;
+  static constexpr int R[1] = {16};
+};
+template <bool FEW>
+struct Plan<4096, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {16, 16, 16};
+};
+template <bool FEW>
+struct Plan<114, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {2, 3, 19};
+};
+
+__device__ __forceinline__ int makhoul_src(int t, int N) { return (2 * t < N) ? 2 * t : 2 * N - 1 - 2 * t; }
+
+// Direct DFT of odd length R (K = 114: R = 19) with roots from the K-point
+// twiddle table, by conjugate pairs: with s_q = x_q + x_{R-q}, d_q = x_q -
+// x_{R-q} and theta = 2 pi q p / R,
+//   y_p     = x_0 + sum_q s_q cos(theta) - i sum_q d_q sin(theta)
+//   y_{R-p} = x_0 + sum_q s_q cos(theta) + i sum_q d_q sin(theta),
+// so an output pair costs 4 (R-1)/2 real FMAs and the (R-1)/2 roots are
+// loaded once per butterfly (was R-1 complex products and loads per output).
+template <int R, int K>
+__device__ __forceinline__ void dft_direct(double2 (&x)[R], const double2* __restrict__ tw) {
+  constexpr int H = (R - 1) / 2;
+  double cs[H + 1], sn[H + 1];  // cos / sin (2 pi j / R), j = 1..H
+#pragma unroll
+  for (int j = 1; j <= H; ++j) {
+    const double2 w = __ldg(tw + j * (K / R));  // exp(-2 pi i j / R)
+    cs[j] = w.x;
+    sn[j] = -w.y;
+  }
+  double2 sq[H + 1], dq[H + 1];
+  double2 y0 = x[0];
+#pragma unroll
+  for (int q = 1; q <= H; ++q) {
+    sq[q] = c_add(x[q], x[R - q]);
+    dq[q] = c_sub(x[q], x[R - q]);
+    y0 = c_add(y0, sq[q]);
+  }
+#pragma unroll
+  for (int p = 1; p <= H; ++p) {
+    double2 a = x[0], b = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 1; q <= H; ++q) {
+      const int j = (q * p) % R;
+      const double c = j <= H ? cs[j] : cs[R - j];
+      const double sv = j <= H ? sn[j] : -sn[R - j];
+      a.x = fma(sq[q].x, c, a.x);
+      a.y = fma(sq[q].y, c, a.y);
+      b.x = fma(dq[q].x, sv, b.x);
+      b.y = fma(dq[q].y, sv, b.y);
+    }
+    x[p] = make_double2(a.x + b.y, a.y - b.x);
+    x[R - p] = make_double2(a.x - b.y, a.y + b.x);
+  }
+  x[0] = y0;
+}
+
+template <int R, int K>
+__device__ __forceinline__ void dft(double2 (&x)[R], const double2* __restrict__ tw) {
+  if constexpr (R == 2 || R == 4 || R == 8 || R == 16)
+    Dft<R>::run(x);
+  else if constexpr (R == 3) {
+    // exp(-2 pi i/3) = -1/2 - i sqrt(3)/2
+    constexpr double s3 = 0.86602540378443864676;
+    const double2 a = x[0], b = x[1], c = x[2];
+    const double2 t = c_add(b, c), d = c_sub(b, c);
+    x[0] = c_add(a, t);
+    const double2 u = make_double2(fma(-0.5, t.x, a.x), fma(-0.5, t.y, a.y));
+    // -i sqrt3/2 d
+    const double2 v = make_double2(s3 * d.y, -s3 * d.x);
+    x[1] = c_add(u, v);
+    x[2] = c_sub(u, v);
+  } else {
+    dft_direct<R, K>(x, tw);
+  }
+}
+
+// One in-place Stockham pass of radix R after NS points are done, over all J
+// interleaved jobs of W[t * J + job].
+template <class C, int R, int NS>
+__device__ __forceinline__ void fft_pass(double2* W, const double2* __restrict__ tw) {
+  constexpr int N = C::N, J = C::J, NR = N / R, ITEMS = NR * J;
+  constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  constexpr int TSTEP = N / (NS * R);
+  double2 v[IPT][R];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) {
+      const int job = it % J, j = it / J, k = j % NS;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        double2 a = W[(j + q * NR) * J + job];
+        if (NS > 1 && q > 0) a = c_mul(a, __ldg(tw + (q * k * TSTEP) % N));
+        v[i][q] = a;
+      }
+      dft<R, N>(v[i], tw);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) {
+      const int job = it % J, j = it / J, k = j % NS;
+      const int outb = (j / NS) * NS * R + k;
+#pragma unroll
+      for (int pp = 0; pp < R; ++pp) W[(outb + pp * NS) * J + job] = v[i][pp];
+    }
+  }
+  __syncthreads();
+}
+
+#ifndef SFEM_MID_DIAG_SKIP
+#define SFEM_MID_DIAG_SKIP 0  // diagnostics builds only: 1 skips the FFT passes, 2 the mixes
+#endif
+template <class C, int P = 0, int NS = 1>
+__device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
+  using PL = Plan<C::N, (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH)>;
+  if constexpr (P < PL::NP && SFEM_MID_DIAG_SKIP != 1) {
+    constexpr int R = PL::R[P];
+    fft_pass<C, R, NS>(W, tw);
+    fft<C, P + 1, NS * R>(W, tw);
+  }
+}
+
+// Item -> (job, index) for the fill / post stages with warps uniform in the
+// job kind: items are grouped pair jobs | middle jobs | nodal jobs, each
+// group index-major with its jobs fastest (consecutive lanes write
+// consecutive W entries of one index: conflict-free).
+template <class C, int NT>
+__device__ __forceinline__ void item_job(int it, int& job, int& t) {
+  constexpr int NP = C::NPAIR, NM = C::Bm, ND = 2 * C::Bh;
+  constexpr int P = NP * NT, PM = (NP + NM) * NT;
+  if (NP > 0 && it < P) {
+    job = it % (NP > 0 ? NP : 1);
+    t = it / (NP > 0 ? NP : 1);
+  } else if (NM > 0 && it < PM) {
+    const int r = it - P;
+    job = NP + r % (NM > 0 ? NM : 1);
+    t = r / (NM > 0 ? NM : 1);
+  } else {
+    const int r = it - PM;
+    job = NP + NM + r % ND;
+    t = r / ND;
+  }
+}
+
+// Out-of-place Stockham passes X -> Y (global-memory work buffers for lines
+// too long for shared memory): one item at a time per thread, no bridge.
+template <class C, int R, int NS>
+__device__ __forceinline__ void fft_pass_oop(const double2* X, double2* Y, const double2* __restrict__ tw) {
+  constexpr int N = C::N, J = C::J, NR = N / R, ITEMS = NR * J;
+  constexpr int TSTEP = N / (NS * R);
+  for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+    const int job = it % J, j = it / J, k = j % NS;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      double2 a = X[(j + q * NR) * J + job];
+      if (NS > 1 && q > 0) a = c_mul(a, __ldg(tw + (q * k * TSTEP) % N));
+      v[q] = a;
+    }
+    dft<R, N>(v, tw);
+    const int outb = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int pp = 0; pp < R; ++pp) Y[(outb + pp * NS) * J + job] = v[pp];
+  }
+  __syncthreads();
+}
+
+// Returns the buffer holding the result.
+template <class C, int P = 0, int NS = 1>
+__device__ __forceinline__ double2* fft_oop(double2* X, double2* Y, const double2* __restrict__ tw) {
+  using PL = Plan<C::N, (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH)>;
+  if constexpr (P < PL::NP) {
+    constexpr int R = PL::R[P];
+    fft_pass_oop<C, R, NS>(X, Y, tw);
+    return fft_oop<C, P + 1, NS * R>(Y, X, tw);
+  } else {
+    return X;
+  }
+}
+
+// ------------------------------------------------------------ forward fill
+// W[t][job] from the tile (bridge), plus the chunked centre partial sums.
+// SEP: the tile T is a separate staging buffer, so W is written directly
+// (no bridge); otherwise T aliases the region R.
+template <class C, bool SEP = false>
+__device__ __forceinline__ void forward_fill(const double* T, double* R, double* PS, const double2* __restrict__ om) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  double2* W = reinterpret_cast<double2*>(R);
+  double2 z[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    z[i] = make_double2(0.0, 0.0);
+    if (it < ITEMS) {
+      int job, tt;
+      item_job<C, N>(it, job, tt);
+      if (job < NPAIR) {
+        const int ii = job / B, b = job % B;
+        const int e = makhoul_src(tt, N);
+        const double ri = T[C::ix(e * n + ii, b)], rr = T[C::ix(e * n + m - 1 - ii, b)];
+        double gg = ri + rr;
+        if (e & 1) gg = -gg;
+        z[i] = make_double2(ri - rr, gg);
+      } else if (job < NPAIR + C::Bm) {
+        const int b = job - NPAIR, b2 = b + Bh;
+        const int e = makhoul_src(tt, N);
+        double g1 = T[C::ix(e * n + C::half, b)];
+        double g2 = b2 < B ? T[C::ix(e * n + C::half, b2)] : 0.0;
+        if (e & 1) {
+          g1 = -g1;
+          g2 = -g2;
+        }
+        z[i] = make_double2(g1, g2);
+      } else {
+        const int jb = job - NPAIR - C::Bm;
+        const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+        if (tt > 0) {
+          z[i] = make_double2(T[C::ix(tt * n - 1, b)], b2 < B ? T[C::ix(tt * n - 1, b2)] : 0.0);
+          if (which) z[i] = c_mul(z[i], __ldg(om + tt));
+        }
+      }
+      if (SEP) W[tt * J + job] = z[i];
+    }
+  }
+  // centre partials: sum (i, b) over elements [c * ECH, (c+1) * ECH)
+  double part = 0.0;
+  const int cit = threadIdx.x;
+  if constexpr (C::NCEN > 0) {
+    if (cit < C::CHUNKS * C::NCEN) {
+      const int s = cit % C::NCEN, c = cit / C::NCEN;
+      const int ii = s / B, b = s % B;
+      const int e0 = c * C::ECH, e1 = min(N, e0 + C::ECH);
+      for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ix(e * n + m - 1 - ii, b)] : T[C::ix(e * n + ii, b)];
+    }
+  }
+  if (!SEP) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int it = threadIdx.x + i * C::THREADS;
+      if (it < ITEMS) {
+        int job, tt;
+        item_job<C, N>(it, job, tt);
+        W[tt * J + job] = z[i];
+      }
+    }
+  }
+  if (C::NCEN > 0 && cit < C::CHUNKS * C::NCEN) PS[cit] = part;  // NCEN = 0: no centre (n = 1)
+  __syncthreads();
+}
+
+// C0[s] = sum over chunks in order.
+template <class C>
+__device__ __forceinline__ void centre_reduce(const double* PS, double* C0) {
+  for (int s = threadIdx.x; s < C::NCEN; s += C::THREADS) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < C::CHUNKS; ++c) acc += PS[c * C::NCEN + s];
+    C0[s] = acc;
+  }
+}
+
+// ------------------------------------------------------------ forward post
+// FFT results -> slots S (at tile positions m + (k-1) n + s), bridge.
+// One post item: up to two slot values and their tile indices (-1: none).
+struct Out2 {
+  double v1, v2;
+  int i1, i2;
+};
+
+template <class C>
+__device__ __forceinline__ Out2 forward_post_item(const double2* Z, int it, const double2* __restrict__ mk) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  Out2 o{0.0, 0.0, -1, -1};
+  int job, k;
+  item_job<C, N - 1>(it, job, k);
+  k += 1;
+  if (job < NPAIR + C::Bm) {
+    const double2 zk = Z[k * J + job], zc = Z[(N - k) * J + job];
+    const double2 w = __ldg(mk + k);
+    // r1 = Re(mk_k V1), r2 = Re(mk_k V2), V1 = (Z_k + conj Z_{N-k})/2, V2 = (Z_k - conj Z_{N-k})/(2i)
+    const double a1 = 0.5 * (zk.x + zc.x), b1 = 0.5 * (zk.y - zc.y);
+    const double a2 = 0.5 * (zk.y + zc.y), b2 = -0.5 * (zk.x - zc.x);
+    o.v1 = w.x * a1 - w.y * b1;
+    o.v2 = w.x * a2 - w.y * b2;
+    if (job < NPAIR) {
+      const int ii = job / B, b = job % B;
+      o.i1 = C::ix(m + (k - 1) * n + 1 + C::ne + ii, b);  // H_k
+      o.i2 = C::ix(m + (N - k - 1) * n + 1 + ii, b);      // G_{N-k}
+    } else {
+      const int b = job - NPAIR, bb = b + Bh;
+      o.i1 = C::ix(m + (N - k - 1) * n + 1 + C::half, b);
+      if (bb < B) o.i2 = C::ix(m + (N - k - 1) * n + 1 + C::half, bb);
+    }
+  } else {
+    const int jb = job - NPAIR - C::Bm;
+    const int b = jb % Bh, which = jb / Bh, bb = b + Bh;
+    if ((k & 1) == which) {
+      double2 d;
+      if (!which) {
+        const int kp = k / 2;
+        d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
+      } else {
+        const int kp = (k - 1) / 2;
+        d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
+      }
+      // X = d / (2i)
+      o.v1 = 0.5 * d.y;
+      o.v2 = -0.5 * d.x;
+      o.i1 = C::ix(m + (k - 1) * n, b);
+      if (bb < B) o.i2 = C::ix(m + (k - 1) * n, bb);
+    }
+  }
+  return o;
+}
+
+// Runs ITEMS items of f into the tile R: bridged (all items loaded, barrier,
+// all stored) when the source aliases R, direct otherwise.
+template <class C, bool SEP, int ITEMS, class F>
+__device__ __forceinline__ void run_out2(double* R, F f) {
+  if constexpr (SEP) {
+    for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+      const Out2 o = f(it);
+      if (o.i1 >= 0) R[o.i1] = o.v1;
+      if (o.i2 >= 0) R[o.i2] = o.v2;
+    }
+  } else {
+    constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+    Out2 o[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int it = threadIdx.x + i * C::THREADS;
+      o[i] = it < ITEMS ? f(it) : Out2{0.0, 0.0, -1, -1};
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      if (o[i].i1 >= 0) R[o[i].i1] = o[i].v1;
+      if (o[i].i2 >= 0) R[o[i].i2] = o[i].v2;
+    }
+  }
+  __syncthreads();
+}
+
+// FFT results -> slots S (at tile positions m + (k-1) n + s).
+template <class C, bool SEP = false>
+__device__ __forceinline__ void forward_post(const double2* Z, double* R, const double2* __restrict__ mk) {
+  run_out2<C, SEP, (C::N - 1) * C::J>(R, [&](int it) { return forward_post_item<C>(Z, it, mk); });
+}
+
+// ------------------------------------------------------------ mixes
+// Symbol divide c / d (d > 0): MUFU reciprocal seed, one Newton step, one
+// residual correction of the quotient -- within 1 ulp of IEEE division (the
+// fast kernels' sym_div, measured over 2^30 quotients by tools/div_ulp.cu)
+// at a third of the instructions of the IEEE division sequence.
+#ifndef SFEM_MID_FAST_DIV
+#define SFEM_MID_FAST_DIV 1
+#endif
+__device__ __forceinline__ double mid_div(double c, double d) {
+#if SFEM_MID_FAST_DIV
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  const double q = c * r;
+  return fma(fma(-d, q, c), r, q);
+#else
+  return c / d;
+#endif
+}
+
+// Per (k >= 1, line) item, in place at tile positions m + (k-1) n + [0, n):
+//   MODE kForward:             c = Mf v
+//   MODE kInverse:             u = Mi c
+//   MODE kForwardDivideInverse u = Mi (Mf v / denom)
+// Items (K-1)*B .. (K-1)*B + B - 1 are the centre blocks of the lines.
+//
+// SFEM_MID_KMIX (default): the matrices are the k-contiguous copies mixT_w/d
+// ([l][s][k]) and mixT_i ([s][l][k]).  Items run b-fastest, so a warp covers
+// 32/B consecutive frequencies and one matrix load is one or a few 32-byte
+// sectors instead of 32/B of them (the per-frequency [k][l][s] layout).
+// C3 (n=9, K=1024: 0.66 MB per matrix set, not L1-resident): solve 8.30 ->
+// 4.92 ms; C5 n=4 / n=9: -6 % / -5 % (bitwise-identical results).
+template <class C, int MODE>
+__device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, const double* __restrict__ mixF,
+                                    const double* __restrict__ e0F, const double* __restrict__ mixI,
+                                    const double* __restrict__ e0I, const double* base,
+                                    const double* __restrict__ eig, double f_last) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B;
+#if SFEM_MID_KMIX
+#define MIDX(a, b) (((a) * n + (b)) * N)
+#else
+#define MIDX(a, b) ((a) * n + (b))
+#endif
+  constexpr int ITEMS = (SFEM_MID_DIAG_SKIP == 2) ? 0 : (N - 1) * B + B;
+  for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+    if (it < (N - 1) * B) {
+      const int k = 1 + it / B, b = it % B;
+      double* p = T + C::ix(m + (k - 1) * n, b);
+      const double* pin = Tin + C::ix(m + (k - 1) * n, b);
+      double v[n], c[n];
+#pragma unroll
+      for (int s = 0; s < n; ++s) v[s] = pin[s * C::PSTR];
+      if (MODE != kInverse) {
+#if SFEM_MID_KMIX
+        const double* M = mixF + k;
+        v[0] *= 2.0;  // the nodal column of mixT_* carries a factor 1/2 (exact)
+#else
+        const double* M = mixF + static_cast<size_t>(k - 1) * n * n;
+#endif
+#pragma unroll
+        for (int l = 0; l < n; ++l) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < n; ++s) acc = fma(__ldg(M + MIDX(l, s)), v[s], acc);
+          if (MODE == kForwardDivideInverse) acc = mid_div(acc, base[b] + f_last * __ldg(eig + m + (k - 1) * n + l));
+          c[l] = acc;
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < n; ++l) c[l] = v[l];
+      }
+      if (MODE != kForward) {
+#if SFEM_MID_KMIX
+        const double* M = mixI + k;
+#else
+        const double* M = mixI + static_cast<size_t>(k - 1) * n * n;
+#endif
+#pragma unroll
+        for (int s = 0; s < n; ++s) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < n; ++l) acc = fma(__ldg(M + MIDX(s, l)), c[l], acc);
+          v[s] = acc;
+        }
+#if SFEM_MID_KMIX
+        v[0] *= 2.0;  // nodal row of mixT_i carries 1/2 (exact)
+#endif
+#pragma unroll
+        for (int s = 0; s < n; ++s) p[s * C::PSTR] = v[s];
+      } else {
+#pragma unroll
+        for (int l = 0; l < n; ++l) p[l * C::PSTR] = c[l];
+      }
+    } else if (m > 0) {
+      // centre block of line b: coefficients l < m (k = 0)
+      const int b = it - (N - 1) * B;
+      double c[m > 0 ? m : 1];
+      if (MODE != kInverse) {
+#pragma unroll
+        for (int l = 0; l < m; ++l) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < m; ++i) acc = fma(C0[i * B + b], __ldg(e0F + i * m + l), acc);
+          if (MODE == kForwardDivideInverse) acc = mid_div(acc, base[b] + f_last * __ldg(eig + l));
+          c[l] = acc;
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < m; ++l) c[l] = Tin[C::ix(l, b)];
+      }
+      if (MODE == kForward) {
+#pragma unroll
+        for (int l = 0; l < m; ++l) T[C::ix(l, b)] = c[l];
+      } else {
+        // centre of the synthesis: C0[i] = sum_l e0_inv[i][l] c[l]
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < m; ++l) acc = fma(__ldg(e0I + i * m + l), c[l], acc);
+          C0[i * B + b] = acc;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+#undef MIDX
+
+// ------------------------------------------------------------ inverse fill
+template <class C>
+__device__ __forceinline__ double2 inverse_fill_item(const double* T, int it, int& widx,
+                                                     const double2* __restrict__ mkh, const double2* __restrict__ om) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  double2 z = make_double2(0.0, 0.0);
+  int job, tt;
+  item_job<C, N>(it, job, tt);
+  widx = tt * J + job;
+  if (tt > 0) {
+    if (job < NPAIR + C::Bm) {
+      const double2 w = __ldg(mkh + tt);
+      double ax, ar, bx, br;  // V1 = w (ax - i ar), V2 = w (bx - i br)
+      if (job < NPAIR) {
+        const int ii = job / B, b = job % B;
+        ax = T[C::ix(m + (tt - 1) * n + 1 + C::ne + ii, b)];
+        ar = T[C::ix(m + (N - tt - 1) * n + 1 + C::ne + ii, b)];
+        bx = T[C::ix(m + (N - tt - 1) * n + 1 + ii, b)];
+        br = T[C::ix(m + (tt - 1) * n + 1 + ii, b)];
+      } else {
+        const int b = job - NPAIR, b2 = b + Bh;
+        ax = T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b)];
+        ar = T[C::ix(m + (tt - 1) * n + 1 + C::half, b)];
+        bx = b2 < B ? T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b2)] : 0.0;
+        br = b2 < B ? T[C::ix(m + (tt - 1) * n + 1 + C::half, b2)] : 0.0;
+      }
+      const double2 v1 = c_mul(w, make_double2(ax, -ar));
+      const double2 v2 = c_mul(w, make_double2(bx, -br));
+      // conj(V1 + i V2): the inverse DFT runs as a forward FFT of the conjugate
+      z = make_double2(v1.x - v2.y, -(v1.y + v2.x));
+    } else {
+      const int jb = job - NPAIR - C::Bm;
+      const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+      z = make_double2(T[C::ix(m + (tt - 1) * n, b)], b2 < B ? T[C::ix(m + (tt - 1) * n, b2)] : 0.0);
+      if (which) z = c_mul(z, __ldg(om + tt));
+    }
+  }
+  return z;
+}
+
+// Slots (tile) -> W; bridged when W aliases the tile.
+template <class C, bool SEP = false>
+__device__ __forceinline__ void inverse_fill(const double* T, double2* W, const double2* __restrict__ mkh,
+                                             const double2* __restrict__ om) {
+  constexpr int ITEMS = C::N * C::J;
+  if constexpr (SEP) {
+    for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
+      int widx;
+      const double2 z = inverse_fill_item<C>(T, it, widx, mkh, om);
+      W[widx] = z;
+    }
+  } else {
+    constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+    double2 z[IPT];
+    int wi[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int it = threadIdx.x + i * C::THREADS;
+      wi[i] = -1;
+      if (it < ITEMS) z[i] = inverse_fill_item<C>(T, it, wi[i], mkh, om);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+      if (wi[i] >= 0) W[wi[i]] = z[i];
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ inverse post
+template <class C>
+__device__ __forceinline__ Out2 inverse_post_item(const double2* Z, int it, const double* C0) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
+  Out2 o{0.0, 0.0, -1, -1};
+  int job, tt;
+  item_job<C, N>(it, job, tt);
+  if (job < NPAIR + C::Bm) {
+    const double2 u = Z[tt * J + job];
+    const double ure = u.x, uim = -u.y;
+    const int e = makhoul_src(tt, N);
+    const bool odd = e & 1;
+    if (job < NPAIR) {
+      const int ii = job / B, b = job % B;
+      const double ev = odd ? -uim : uim;
+      const double ci = odd ? -C0[(m - 1 - ii) * B + b] : C0[ii * B + b];
+      const double cr = odd ? -C0[ii * B + b] : C0[(m - 1 - ii) * B + b];
+      o.v1 = ci + ev + ure;
+      o.v2 = cr + ev - ure;
+      o.i1 = C::ix(e * n + ii, b);
+      o.i2 = C::ix(e * n + m - 1 - ii, b);
+    } else {
+      const int b = job - NPAIR, b2 = b + Bh;
+      constexpr int hc = C::half;
+      const double c1 = odd ? -C0[hc * B + b] : C0[hc * B + b];
+      o.v1 = c1 + (odd ? -ure : ure);
+      o.i1 = C::ix(e * n + hc, b);
+      if (b2 < B) {
+        const double c2 = odd ? -C0[hc * B + b2] : C0[hc * B + b2];
+        o.v2 = c2 + (odd ? -uim : uim);
+        o.i2 = C::ix(e * n + hc, b2);
+      }
+    }
+  } else {
+    const int jb = job - NPAIR - C::Bm;
+    const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+    const int j = tt;
+    if (j >= 1 && j <= N - 1 && (j & 1) == which) {
+      double2 d;
+      if (!which) {
+        const int kp = j / 2;
+        d = c_sub(Z[(N - kp) * J + job], Z[kp * J + job]);
+      } else {
+        const int kp = (j - 1) / 2;
+        d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
+      }
+      o.v1 = 0.5 * d.y;
+      o.i1 = C::ix(j * n - 1, b);
+      if (b2 < B) {
+        o.v2 = -0.5 * d.x;
+        o.i2 = C::ix(j * n - 1, b2);
+      }
+    }
+  }
+  return o;
+}
+
+// FFT results + centre -> the line tile R.
+template <class C, bool SEP = false>
+__device__ __forceinline__ void inverse_post(const double2* Z, double* R, const double* C0) {
+  run_out2<C, SEP, C::N * C::J>(R, [&](int it) { return inverse_post_item<C>(Z, it, C0); });
+}
+
+// ------------------------------------------------------------ kernel
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+// Strided tiles whose B lines are adjacent, 16-byte aligned and all present:
+// each position row (B doubles, contiguous in both places) moves as B/2
+// 16-byte copies / stores instead of B 8-byte ones.
+template <class C>
+__device__ __forceinline__ bool vec_tile(const long long* off, int Bv, long long ps, const double* src,
+                                         const double* dst) {
+  if constexpr (C::ROWS || (C::B & 1)) return false;
+  bool ok = Bv == C::B && (off[0] & 1) == 0 && (ps & 1) == 0 &&
+            ((reinterpret_cast<unsigned long long>(src) | reinterpret_cast<unsigned long long>(dst)) & 15) == 0;
+#pragma unroll
+  for (int b = 1; b < C::B; ++b) ok = ok && off[b] == off[0] + b;
+  return ok;
+}
+
+template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
+__global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 registers
+    sweep_mid(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
+              const double* __restrict__ e0F) {
+  using C = Cfg<NN, K, BB, TH, ROWS>;
+  constexpr int B = C::B, L = C::L;
+  extern __shared__ __align__(16) double smem[];
+  double* R = smem;
+  double* C0 = smem + C::C0_OFF;
+  double* PS = smem + C::PS_OFF;
+  double* base = smem + C::BASE_OFF;
+  __shared__ long long off[B];
+  SFEM_PT_DECL;
+  SFEM_PT(0);
+
+  const long long l0 = static_cast<long long>(blockIdx.x) * B;
+  const int Bv = static_cast<int>(min(static_cast<long long>(B), ls.nlines - l0));
+  if (threadIdx.x < B) {
+    const int b = threadIdx.x;
+    const long long l = l0 + b;
+    const long long r = l / ls.ninner;
+    off[b] = l < ls.nlines ? (r / ls.n1) * ls.os2 + (r % ls.n1) * ls.os1 + (l % ls.ninner) * ls.is : 0;
+    if (MODE == kForwardDivideInverse) {
+      // base = shift + sum_{i<N-1} f_i lambda_i (poisson.cpp:586-590 order)
+      long long rem = l < ls.nlines ? l : 0;
+      double terms[kMaxDim];
+#pragma unroll
+      for (int i = kMaxDim - 1; i >= 0; --i) {
+        terms[i] = 0.0;
+        if (i < sym.nlead) {
+          const long long a = rem % sym.lead_ext[i];
+          rem /= sym.lead_ext[i];
+          terms[i] = sym.lead_f[i] * sym.lead_eig[i][a];
+        }
+      }
+      double s = sym.shift;
+#pragma unroll
+      for (int i = 0; i < kMaxDim; ++i)
+        if (i < sym.nlead) s += terms[i];
+      base[b] = s;
+    }
+  }
+  __syncthreads();
+
+  // tile load, all copies in flight at once (phantom lines zero-filled)
+  const long long ps = ls.ps;
+  const bool vec = vec_tile<C>(off, Bv, ps, ls.src, ls.dst);
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      cp_async8(R + C::ix(pos, b), ls.src + off[b] + pos, b < Bv);
+    }
+  } else if (vec) {
+    constexpr int B2 = B / 2;
+    const double* src = ls.src + off[0];
+    for (int it = threadIdx.x; it < L * B2; it += TH) {
+      const int pos = it / B2, b2 = it - pos * B2;
+      cp_async16(R + 2 * it, src + pos * ps + 2 * b2);
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      cp_async8(R + it, ls.src + off[b] + pos * ps, b < Bv);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  SFEM_PT(1);
+
+  if (MODE != kInverse) {
+    forward_fill<C>(R, R, PS, t.om);
+    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    centre_reduce<C>(PS, C0);  // PS / C0 are outside the region
+    forward_post<C>(reinterpret_cast<const double2*>(R), R, t.mk);
+  }
+  SFEM_PT(2);
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  SFEM_PT(3);
+  if (MODE != kForward) {
+    inverse_fill<C>(R, reinterpret_cast<double2*>(R), t.mkh, t.om);
+    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    inverse_post<C>(reinterpret_cast<const double2*>(R), R, C0);
+  }
+  SFEM_PT(4);
+
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      if (b < Bv) ls.dst[off[b] + pos] = R[C::ix(pos, b)];
+    }
+  } else if (vec) {
+    constexpr int B2 = B / 2;
+    double* dst = ls.dst + off[0];
+    for (int it = threadIdx.x; it < L * B2; it += TH) {
+      const int pos = it / B2, b2 = it - pos * B2;
+      *reinterpret_cast<double2*>(dst + pos * ps + 2 * b2) = *reinterpret_cast<const double2*>(R + 2 * it);
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      if (b < Bv) ls.dst[off[b] + pos * ps] = R[it];
+    }
+  }
+  SFEM_PT(5);
+  SFEM_PT_FLUSH(20 + MODE);
+}
+
+
+// Lines too long for an FFT buffer in shared memory (C2: n=4, K=4096): the
+// tile stays in shared memory, the J*K complex FFT work of the CTA lives in
+// two slices of a global scratch array (L2-resident while the CTA runs; the
+// slices are discarded from L2 at exit, so they never reach HBM).
+template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
+__global__ void __launch_bounds__(TH, 1)
+    sweep_mid_gw(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
+                 const double* __restrict__ e0F, double* gwork) {
+  using C = Cfg<NN, K, BB, TH, ROWS, true>;
+  constexpr int B = C::B, L = C::L, JK = C::J * C::N;
+  extern __shared__ __align__(16) double smem[];
+  double* R = smem;  // tile and slots (REGION >= TD)
+  double* C0 = smem + C::C0_OFF;
+  double* PS = smem + C::PS_OFF;
+  double* base = smem + C::BASE_OFF;
+  __shared__ long long off[B];
+  double2* W0 = reinterpret_cast<double2*>(gwork) + static_cast<size_t>(blockIdx.x) * 2 * JK;
+  double2* W1 = W0 + JK;
+
+  const long long l0 = static_cast<long long>(blockIdx.x) * B;
+  const int Bv = static_cast<int>(min(static_cast<long long>(B), ls.nlines - l0));
+  if (threadIdx.x < B) {
+    const int b = threadIdx.x;
+    const long long l = l0 + b;
+    const long long r = l / ls.ninner;
+    off[b] = l < ls.nlines ? (r / ls.n1) * ls.os2 + (r % ls.n1) * ls.os1 + (l % ls.ninner) * ls.is : 0;
+    if (MODE == kForwardDivideInverse) {
+      long long rem = l < ls.nlines ? l : 0;
+      double terms[kMaxDim];
+#pragma unroll
+      for (int i = kMaxDim - 1; i >= 0; --i) {
+        terms[i] = 0.0;
+        if (i < sym.nlead) {
+          const long long a = rem % sym.lead_ext[i];
+          rem /= sym.lead_ext[i];
+          terms[i] = sym.lead_f[i] * sym.lead_eig[i][a];
+        }
+      }
+      double sb = sym.shift;
+#pragma unroll
+      for (int i = 0; i < kMaxDim; ++i)
+        if (i < sym.nlead) sb += terms[i];
+      base[b] = sb;
+    }
+  }
+  __syncthreads();
+  const long long ps = ls.ps;
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      cp_async8(R + C::ix(pos, b), ls.src + off[b] + pos, b < Bv);
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      cp_async8(R + it, ls.src + off[b] + pos * ps, b < Bv);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  if (MODE != kInverse) {
+    forward_fill<C, true>(R, reinterpret_cast<double*>(W0), PS, t.om);
+    const double2* Z = fft_oop<C>(W0, W1, t.tw);
+    centre_reduce<C>(PS, C0);
+    forward_post<C, true>(Z, R, t.mk);
+  }
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  if (MODE != kForward) {
+    inverse_fill<C, true>(R, W0, t.mkh, t.om);
+    const double2* Z = fft_oop<C>(W0, W1, t.tw);
+    inverse_post<C, true>(Z, R, C0);
+  }
+  if (ROWS) {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int b = it / L, pos = it - b * L;
+      if (b < Bv) ls.dst[off[b] + pos] = R[C::ix(pos, b)];
+    }
+  } else {
+    for (int it = threadIdx.x; it < L * B; it += TH) {
+      const int pos = it / B, b = it % B;
+      if (b < Bv) ls.dst[off[b] + pos * ps] = R[it];
+    }
+  }
+  // the work slices are dead: drop them from L2 without write-back
+  char* wb = reinterpret_cast<char*>(W0);
+  for (int i = threadIdx.x; i < (2 * JK * 16) / 128; i += TH)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(wb + static_cast<size_t>(i) * 128) : "memory");
+}
+
+template <int NN, int K, int BB, int TH>
+cudaError_t launch_gw(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
+                      double* gwork, cudaStream_t stream) {
+  const double* mixF = SFEM_MID_KMIX ? (analysis == kDirect ? t.mixT_d : t.mixT_w)
+                                     : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
+  const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
+  SymbolInfo s{};
+  if (sym) s = *sym;
+  const dim3 grid(static_cast<unsigned>((ls.nlines + BB - 1) / BB));
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto kern, size_t smem) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (err != cudaSuccess) return;
+    kern<<<grid, TH, smem, stream>>>(t, ls, s, mixF, e0F, gwork);
+    err = cudaGetLastError();
+  };
+  // shared memory: the tile only (the FFT buffers are global)
+  constexpr size_t SR = Cfg<NN, K, BB, TH, true, true>::SMEM, SS = Cfg<NN, K, BB, TH, false, true>::SMEM;
+  if (mode == kForwardDivideInverse) {
+    if (!ls.contiguous) return cudaErrorNotSupported;
+    go(sweep_mid_gw<NN, K, BB, TH, kForwardDivideInverse, true>, SR);
+  } else if (mode == kForward) {
+    ls.contiguous ? go(sweep_mid_gw<NN, K, BB, TH, kForward, true>, SR)
+                  : go(sweep_mid_gw<NN, K, BB, TH, kForward, false>, SS);
+  } else {
+    ls.contiguous ? go(sweep_mid_gw<NN, K, BB, TH, kInverse, true>, SR)
+                  : go(sweep_mid_gw<NN, K, BB, TH, kInverse, false>, SS);
+  }
+  return err;
+}
+
+template <int NN, int K, int BB, int TH>
+cudaError_t launch(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
+                   cudaStream_t stream) {
+  const double* mixF = SFEM_MID_KMIX ? (analysis == kDirect ? t.mixT_d : t.mixT_w)
+                                     : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
+  const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
+  SymbolInfo s{};
+  if (sym) s = *sym;
+  const dim3 grid(static_cast<unsigned>((ls.nlines + BB - 1) / BB));
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto kern, size_t smem) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (err != cudaSuccess) return;
+    kern<<<grid, TH, smem, stream>>>(t, ls, s, mixF, e0F);
+    err = cudaGetLastError();
+  };
+  using CR = Cfg<NN, K, BB, TH, true>;
+  using CS = Cfg<NN, K, BB, TH, false>;
+  if (mode == kForwardDivideInverse) {
+    if (!ls.contiguous) return cudaErrorNotSupported;
+    go(sweep_mid<NN, K, BB, TH, kForwardDivideInverse, true>, CR::SMEM);
+  } else if (mode == kForward) {
+    ls.contiguous ? go(sweep_mid<NN, K, BB, TH, kForward, true>, CR::SMEM)
+                  : go(sweep_mid<NN, K, BB, TH, kForward, false>, CS::SMEM);
+  } else {
+    ls.contiguous ? go(sweep_mid<NN, K, BB, TH, kInverse, true>, CR::SMEM)
+                  : go(sweep_mid<NN, K, BB, TH, kInverse, false>, CS::SMEM);
+  }
+  return err;
+}
+
+// Tile shape for the general (n, K) instantiations: the most lines per tile
+// (8, 4, 2) whose shared region fits two 256-thread CTAs per SM, else two
+// lines with one 512-thread CTA per SM, else none (generic kernels).
+template <int NN, int K>
+struct AutoShape {
+  template <int BB, int TH>
+  static constexpr bool fits(size_t budget) {
+    return Cfg<NN, K, BB, TH, true>::SMEM <= budget && Cfg<NN, K, BB, TH, false>::SMEM <= budget;
+  }
+  static constexpr int B = fits<8, 256>(110 * 1024) ? 8 : fits<4, 256>(110 * 1024) ? 4
+                           : fits<2, 256>(110 * 1024) ? 2 : fits<2, 512>(220 * 1024) ? 2 : 0;
+  static constexpr int TH = (B == 2 && !fits<2, 256>(110 * 1024)) ? 512 : 256;
+};
+
+// (n, K) served elsewhere: the K = 64 register-FFT kernels (sweep_fast.cu)
+// and the tuned shapes of launch_sweep_mid below.
+template <int NN, int K>
+constexpr bool served_elsewhere() {
+  return (K == 64 && (NN == 2 || NN == 3 || NN == 4 || NN == 5 || NN == 9)) || (NN == 2 && K == 512) ||
+         (NN == 4 && K == 256);
+}
+
+template <int NN, int K>
+cudaError_t launch_auto(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
+                        cudaStream_t stream) {
+  using S = AutoShape<NN, K>;
+  if constexpr (S::B == 0 || served_elsewhere<NN, K>()) {
+    return cudaErrorNotSupported;
+  } else {
+    return launch<NN, K, S::B, S::TH>(t, ls, mode, analysis, sym, stream);
+  }
+}
+
+template <int K>
+cudaError_t launch_auto_n(const DevTable& t, const LineSet& ls, int mode, int analysis, const SymbolInfo* sym,
+                          cudaStream_t stream) {
+  switch (t.n) {
+    case 1: return launch_auto<1, K>(t, ls, mode, analysis, sym, stream);
+    case 2: return launch_auto<2, K>(t, ls, mode, analysis, sym, stream);
+    case 3: return launch_auto<3, K>(t, ls, mode, analysis, sym, stream);
+    case 4: return launch_auto<4, K>(t, ls, mode, analysis, sym, stream);
+    case 5: return launch_auto<5, K>(t, ls, mode, analysis, sym, stream);
+    case 6: return launch_auto<6, K>(t, ls, mode, analysis, sym, stream);
+    case 7: return launch_auto<7, K>(t, ls, mode, analysis, sym, stream);
+    case 8: return launch_auto<8, K>(t, ls, mode, analysis, sym, stream);
+    case 9: return launch_auto<9, K>(t, ls, mode, analysis, sym, stream);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+template <int K>
+bool auto_ok_n(int n) {
+  switch (n) {
+    case 1: return AutoShape<1, K>::B > 0;
+    case 2: return AutoShape<2, K>::B > 0;
+    case 3: return AutoShape<3, K>::B > 0;
+    case 4: return AutoShape<4, K>::B > 0;
+    case 5: return AutoShape<5, K>::B > 0;
+    case 6: return AutoShape<6, K>::B > 0;
+    case 7: return AutoShape<7, K>::B > 0;
+    case 8: return AutoShape<8, K>::B > 0;
+    case 9: return AutoShape<9, K>::B > 0;
+    default: return false;
+  }
+}
+
+}  // namespace mid
+}  // namespace sfem_b200

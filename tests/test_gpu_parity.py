@@ -296,7 +296,10 @@ def test_long_lines_match_oracle(sfem, n, K):
         assert rel_l2(sfem.lines(t, op, x), fn(x, ot)) <= TOL
 
 
-MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024), (4, 4096)]
+MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024), (4, 4096),
+       # general shapes (mid::AutoShape): every order at K in {16, ..., 512}
+       (1, 16), (9, 16), (2, 32), (6, 32), (9, 32), (1, 64), (7, 64), (8, 64), (2, 128), (8, 128), (9, 128),
+       (3, 256), (9, 256), (5, 512), (9, 512)]
 
 
 @pytest.mark.parametrize("n,K", MID)

@@ -6,9 +6,7 @@ set -e
 cd "$(dirname "$0")/../paper_1701_03967_b200"
 mkdir -p ../variants
 while [ $# -ge 2 ]; do
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
-    -Xcompiler -fPIC,-fopenmp,-O3 $2 -shared -o ../variants/$1.so \
-    csrc/*.cu csrc/*.cpp -lgomp > ../variants/$1.log 2>&1 &
+  (make -j16 BUILD=../variants/$1.build OUT=../variants/$1.so EXTRA="$2" > ../variants/$1.log 2>&1 && rm -rf ../variants/$1.build) &
   shift 2
 done
 wait
