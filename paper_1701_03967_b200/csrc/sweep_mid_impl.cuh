@@ -1043,7 +1043,7 @@ struct AutoShape {
 // and the tuned shapes of launch_sweep_mid below.
 template <int NN, int K>
 constexpr bool served_elsewhere() {
-  return (K == 64 && (NN == 2 || NN == 3 || NN == 4 || NN == 5 || NN == 9)) || (NN == 2 && K == 512) ||
+  return (K == 64 && NN >= 2) || (NN == 2 && K == 512) ||
          (NN == 4 && K == 256);
 }
 

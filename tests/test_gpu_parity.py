@@ -206,7 +206,7 @@ def test_config1_matches_reference_cpu_solver(sfem):
     assert rel_l2(u, want) <= TOL
 
 
-@pytest.mark.parametrize("n", [2, 3, 4, 5, 9])
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 8, 9])
 def test_fast_kernels_match_generic_and_oracle(sfem, n, monkeypatch):
     # K = 64 runs the register-FFT kernels (sweep_fast.cu); SFEM_GENERIC=1 forces
     # the shared-memory Stockham kernels (sweep.cu).  Both must meet the oracle.
@@ -298,7 +298,7 @@ def test_long_lines_match_oracle(sfem, n, K):
 
 MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024), (4, 4096),
        # general shapes (mid::AutoShape): every order at K in {16, ..., 512}
-       (1, 16), (9, 16), (2, 32), (6, 32), (9, 32), (1, 64), (7, 64), (8, 64), (2, 128), (8, 128), (9, 128),
+       (1, 16), (9, 16), (2, 32), (6, 32), (9, 32), (1, 64), (2, 128), (8, 128), (9, 128),
        (3, 256), (9, 256), (5, 512), (9, 512)]
 
 
