@@ -1,6 +1,6 @@
 // Dispatch of the mid-length line kernels (templates in sweep_mid_impl.cuh):
 // the tuned shapes are instantiated here, the general power-of-two shapes in
-// sweep_mid_k{16,...,512}.cu (one translation unit per K, built in parallel).
+// sweep_mid_k{16,...,2048}.cu (one translation unit per K, built in parallel).
 #include "sweep_mid_impl.cuh"
 
 namespace sfem_b200 {
@@ -20,6 +20,10 @@ extern template cudaError_t launch_auto_n<256>(const DevTable&, const LineSet&, 
                                                  cudaStream_t);
 extern template cudaError_t launch_auto_n<512>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<1024>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<2048>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
 
 }  // namespace mid
 
@@ -63,6 +67,8 @@ bool mid_auto(int n, int K) {
     case 128: return mid::auto_ok_n<128>(n);
     case 256: return mid::auto_ok_n<256>(n);
     case 512: return mid::auto_ok_n<512>(n);
+    case 1024: return n != 1 && n != 9 && mid::auto_ok_n<1024>(n);
+    case 2048: return mid::auto_ok_n<2048>(n);
     default: return false;
   }
 #else
@@ -110,6 +116,8 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int
       case 128: return mid::launch_auto_n<128>(t, ls, mode, analysis, sym, stream);
       case 256: return mid::launch_auto_n<256>(t, ls, mode, analysis, sym, stream);
       case 512: return mid::launch_auto_n<512>(t, ls, mode, analysis, sym, stream);
+      case 1024: return mid::launch_auto_n<1024>(t, ls, mode, analysis, sym, stream);
+      case 2048: return mid::launch_auto_n<2048>(t, ls, mode, analysis, sym, stream);
       default: break;
     }
   }

@@ -95,6 +95,11 @@ struct Plan<1024, FEW> {
 #endif
 };
 template <bool FEW>
+struct Plan<2048, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {16, 16, 8};
+};
+template <bool FEW>
 struct Plan<512, FEW> {
   static constexpr int NP = 3;
   static constexpr int R[3] = {8, 8, 8};
@@ -238,7 +243,7 @@ __device__ __forceinline__ void fft_pass(double2* W, const double2* __restrict__
 }
 
 #ifndef SFEM_MID_DIAG_SKIP
-#define SFEM_MID_DIAG_SKIP 0  // diagnostics builds only: 1 skips the FFT passes, 2 the mixes
+#define SFEM_MID_DIAG_SKIP 0  // diagnostics builds only: 1 skips the FFT passes, 2 the mixes, 3 the fills
 #endif
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
@@ -315,7 +320,7 @@ __device__ __forceinline__ double2* fft_oop(double2* X, double2* Y, const double
 template <class C, bool SEP = false>
 __device__ __forceinline__ void forward_fill(const double* T, double* R, double* PS, const double2* __restrict__ om) {
   constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
-  constexpr int ITEMS = N * J, IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  constexpr int ITEMS = SFEM_MID_DIAG_SKIP == 3 ? 0 : N * J, IPT = (N * J + C::THREADS - 1) / C::THREADS;
   double2* W = reinterpret_cast<double2*>(R);
   double2 z[IPT];
 #pragma unroll
@@ -653,7 +658,7 @@ __device__ __forceinline__ double2 inverse_fill_item(const double* T, int it, in
 template <class C, bool SEP = false>
 __device__ __forceinline__ void inverse_fill(const double* T, double2* W, const double2* __restrict__ mkh,
                                              const double2* __restrict__ om) {
-  constexpr int ITEMS = C::N * C::J;
+  constexpr int ITEMS = SFEM_MID_DIAG_SKIP == 3 ? 0 : C::N * C::J;
   if constexpr (SEP) {
     for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
       int widx;
@@ -661,7 +666,7 @@ __device__ __forceinline__ void inverse_fill(const double* T, double2* W, const 
       W[widx] = z;
     }
   } else {
-    constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+    constexpr int IPT = (C::N * C::J + C::THREADS - 1) / C::THREADS;
     double2 z[IPT];
     int wi[IPT];
 #pragma unroll
@@ -1043,7 +1048,7 @@ struct AutoShape {
 // and the tuned shapes of launch_sweep_mid below.
 template <int NN, int K>
 constexpr bool served_elsewhere() {
-  return (K == 64 && NN >= 2) || (NN == 2 && K == 512) ||
+  return (K == 64 && NN >= 2) || (NN == 2 && K == 512) || (K == 1024 && (NN == 1 || NN == 9)) ||
          (NN == 4 && K == 256);
 }
 

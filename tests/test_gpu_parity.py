@@ -299,7 +299,7 @@ def test_long_lines_match_oracle(sfem, n, K):
 MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024), (4, 4096),
        # general shapes (mid::AutoShape): every order at K in {16, ..., 512}
        (1, 16), (9, 16), (2, 32), (6, 32), (9, 32), (1, 64), (2, 128), (8, 128), (9, 128),
-       (3, 256), (9, 256), (5, 512), (9, 512)]
+       (3, 256), (9, 256), (5, 512), (9, 512), (4, 1024), (8, 1024), (2, 2048), (5, 2048)]
 
 
 @pytest.mark.parametrize("n,K", MID)
