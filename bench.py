@@ -219,6 +219,32 @@ def run_peer(args, world, rank, local, dist):
     def solve():
         plan.solve(ctx.stream)
 
+    check = None
+    if not args.no_verify:
+        # One distributed solve checked against a single-GPU solve of the same
+        # global load on rank 0 (rank 0's slab depends on every rank's rows
+        # through the two exchanges): a fused exchange that moved the wrong
+        # data is reported and the NCCL path takes over, never timed as is.
+        solve()
+        torch.cuda.synchronize()
+        mine = plan.gather_x()
+        err = 0.0
+        if rank == 0:
+            offs, lens = D.partition_even(plan.extents[0], world)
+            glob = np.concatenate([np.random.default_rng(1000 + r).uniform(-1.0, 1.0, (lens[r], L1, L2))
+                                   for r in range(world)])
+            want, _ = sfem.solve_dof(spec, glob, ctx=ctx)
+            want = want[offs[0]:offs[0] + lens[0]]
+            err = float(np.linalg.norm(mine - want) / np.linalg.norm(want))
+            del glob, want
+        err = max_over_ranks(err, dist, world)
+        if not err <= 1e-11:
+            raise RuntimeError(f"fused NVLink solve differs from the single-GPU solve (rank-0 slab rel-L2 {err:.3e})")
+        check = f"rank-0 slab vs single-GPU solve of the same global load: rel-L2 {err:.2e}"
+        xv[:, :, :L2].copy_(torch.from_numpy(f_local))
+        torch.cuda.synchronize()
+        barrier(dist, world)
+
     for _ in range(args.warmup):
         solve()
     torch.cuda.synchronize()
@@ -265,6 +291,7 @@ def run_peer(args, world, rank, local, dist):
             "config": {"workload": desc, "unknowns": U, "extents": plan.extents,
                        "parallelism": f"slab x{world} (axis-0 slabs; exchanges fused into the sweeps as TMA "
                                       "stores to NVLink peer memory)",
+                       "dist_check": check,
                        "l2_flush": "none needed: tensors > L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
@@ -373,6 +400,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="N > 1: skip the set-up check of the fused exchange against a single-GPU solve")
     ap.add_argument("--dist-mode", default="peer", choices=["peer", "nccl"],
                     help="N > 1: exchanges fused into the sweeps over NVLink peer memory, or NCCL all-to-all")
     ap.add_argument("--dist-single", action="store_true",
