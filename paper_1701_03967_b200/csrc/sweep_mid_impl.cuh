@@ -44,6 +44,12 @@
 #ifndef SFEM_MID_KMIX
 #define SFEM_MID_KMIX 1
 #endif
+// Lines per (k >= 1) mix item, at most SFEM_MID_MIXG (1, 2 or 4; G lines need
+// B % G == 0, and 4 only for n <= 5 to stay in registers).  G lines per item
+// divide the matrix loads per FMA by G.
+#ifndef SFEM_MID_MIXG
+#define SFEM_MID_MIXG 2
+#endif
 
 namespace sfem_b200 {
 namespace mid {
@@ -527,33 +533,55 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 #else
 #define MIDX(a, b) ((a) * n + (b))
 #endif
-  constexpr int ITEMS = (SFEM_MID_DIAG_SKIP == 2) ? 0 : (N - 1) * B + B;
+  // G lines per (k >= 1) item: one matrix load feeds G FMAs (SFEM_MID_MIXG).
+  constexpr int G = (SFEM_MID_MIXG >= 4 && B % 4 == 0 && 4 * n <= 20) ? 4
+                    : (SFEM_MID_MIXG >= 2 && B % 2 == 0)              ? 2
+                                                                       : 1;
+  constexpr int BG = B / G;
+  constexpr int KITEMS = (N - 1) * BG;
+  constexpr int ITEMS = (SFEM_MID_DIAG_SKIP == 2) ? 0 : KITEMS + B;
   for (int it = threadIdx.x; it < ITEMS; it += C::THREADS) {
-    if (it < (N - 1) * B) {
-      const int k = 1 + it / B, b = it % B;
-      double* p = T + C::ix(m + (k - 1) * n, b);
-      const double* pin = Tin + C::ix(m + (k - 1) * n, b);
-      double v[n], c[n];
+    if (it < KITEMS) {
+      const int k = 1 + it / BG, b0 = (it % BG) * G;
+      double v[G][n], c[G][n];
 #pragma unroll
-      for (int s = 0; s < n; ++s) v[s] = pin[s * C::PSTR];
+      for (int g = 0; g < G; ++g) {
+        const double* pin = Tin + C::ix(m + (k - 1) * n, b0 + g);
+#pragma unroll
+        for (int s = 0; s < n; ++s) v[g][s] = pin[s * C::PSTR];
+      }
       if (MODE != kInverse) {
 #if SFEM_MID_KMIX
         const double* M = mixF + k;
-        v[0] *= 2.0;  // the nodal column of mixT_* carries a factor 1/2 (exact)
+#pragma unroll
+        for (int g = 0; g < G; ++g) v[g][0] *= 2.0;  // the nodal column of mixT_* carries a factor 1/2 (exact)
 #else
         const double* M = mixF + static_cast<size_t>(k - 1) * n * n;
 #endif
 #pragma unroll
         for (int l = 0; l < n; ++l) {
-          double acc = 0.0;
+          double acc[G];
 #pragma unroll
-          for (int s = 0; s < n; ++s) acc = fma(__ldg(M + MIDX(l, s)), v[s], acc);
-          if (MODE == kForwardDivideInverse) acc = mid_div(acc, base[b] + f_last * __ldg(eig + m + (k - 1) * n + l));
-          c[l] = acc;
+          for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll
+          for (int s = 0; s < n; ++s) {
+            const double mv = __ldg(M + MIDX(l, s));
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = fma(mv, v[g][s], acc[g]);
+          }
+          if (MODE == kForwardDivideInverse) {
+            const double ev = __ldg(eig + m + (k - 1) * n + l);
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = mid_div(acc[g], base[b0 + g] + f_last * ev);
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) c[g][l] = acc[g];
         }
       } else {
 #pragma unroll
-        for (int l = 0; l < n; ++l) c[l] = v[l];
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int l = 0; l < n; ++l) c[g][l] = v[g][l];
       }
       if (MODE != kForward) {
 #if SFEM_MID_KMIX
@@ -563,23 +591,38 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 #endif
 #pragma unroll
         for (int s = 0; s < n; ++s) {
-          double acc = 0.0;
+          double acc[G];
 #pragma unroll
-          for (int l = 0; l < n; ++l) acc = fma(__ldg(M + MIDX(s, l)), c[l], acc);
-          v[s] = acc;
+          for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll
+          for (int l = 0; l < n; ++l) {
+            const double mv = __ldg(M + MIDX(s, l));
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = fma(mv, c[g][l], acc[g]);
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) v[g][s] = acc[g];
         }
-#if SFEM_MID_KMIX
-        v[0] *= 2.0;  // nodal row of mixT_i carries 1/2 (exact)
-#endif
 #pragma unroll
-        for (int s = 0; s < n; ++s) p[s * C::PSTR] = v[s];
+        for (int g = 0; g < G; ++g) {
+#if SFEM_MID_KMIX
+          v[g][0] *= 2.0;  // nodal row of mixT_i carries 1/2 (exact)
+#endif
+          double* p = T + C::ix(m + (k - 1) * n, b0 + g);
+#pragma unroll
+          for (int s = 0; s < n; ++s) p[s * C::PSTR] = v[g][s];
+        }
       } else {
 #pragma unroll
-        for (int l = 0; l < n; ++l) p[l * C::PSTR] = c[l];
+        for (int g = 0; g < G; ++g) {
+          double* p = T + C::ix(m + (k - 1) * n, b0 + g);
+#pragma unroll
+          for (int l = 0; l < n; ++l) p[l * C::PSTR] = c[g][l];
+        }
       }
     } else if (m > 0) {
       // centre block of line b: coefficients l < m (k = 0)
-      const int b = it - (N - 1) * B;
+      const int b = it - KITEMS;
       double c[m > 0 ? m : 1];
       if (MODE != kInverse) {
 #pragma unroll
