@@ -45,10 +45,13 @@
 #define SFEM_MID_KMIX 1
 #endif
 // Lines per (k >= 1) mix item, at most SFEM_MID_MIXG (1, 2 or 4; G lines need
-// B % G == 0, and 4 only for n <= 5 to stay in registers).  G lines per item
-// divide the matrix loads per FMA by G.
+// B % G == 0; 4 only in the fused kernel and for n <= 5, to stay in
+// registers).  G lines per item divide the matrix loads per FMA by G.
+// Measured (profiles/r1m_mid_mixg*): G = 2 vs 1: C3 -9 %, C5 -4.5..-8 %;
+// G = 4 vs 2: fused C5 sweeps -1.4..-2.7 %, strided ones +1..+7 % (kept
+// at 2 there).
 #ifndef SFEM_MID_MIXG
-#define SFEM_MID_MIXG 2
+#define SFEM_MID_MIXG 4
 #endif
 
 namespace sfem_b200 {
@@ -534,7 +537,7 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 #define MIDX(a, b) ((a) * n + (b))
 #endif
   // G lines per (k >= 1) item: one matrix load feeds G FMAs (SFEM_MID_MIXG).
-  constexpr int G = (SFEM_MID_MIXG >= 4 && B % 4 == 0 && 4 * n <= 20) ? 4
+  constexpr int G = (SFEM_MID_MIXG >= 4 && MODE == kForwardDivideInverse && B % 4 == 0 && 4 * n <= 20) ? 4
                     : (SFEM_MID_MIXG >= 2 && B % 2 == 0)              ? 2
                                                                        : 1;
   constexpr int BG = B / G;
