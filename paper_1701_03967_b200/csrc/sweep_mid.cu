@@ -1,6 +1,7 @@
 // Dispatch of the mid-length line kernels (templates in sweep_mid_impl.cuh):
-// the tuned shapes are instantiated here, the general power-of-two shapes in
-// sweep_mid_k{16,...,2048}.cu (one translation unit per K, built in parallel).
+// the tuned shapes are instantiated here, the general shapes in
+// sweep_mid_k{16,...,2048}.cu (powers of two) and sweep_mid_k{24,...,1000}.cu
+// (3 * 2^j, 5 * 2^j, 2^i * 5^j), one translation unit per K, built in parallel.
 #include "sweep_mid_impl.cuh"
 
 namespace sfem_b200 {
@@ -25,6 +26,32 @@ extern template cudaError_t launch_auto_n<1024>(const DevTable&, const LineSet&,
 extern template cudaError_t launch_auto_n<2048>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
                                                   cudaStream_t);
 
+extern template cudaError_t launch_auto_n<24>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<40>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<48>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<80>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<96>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<100>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<160>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<192>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<200>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<320>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<384>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<768>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
+extern template cudaError_t launch_auto_n<1000>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
+                                                  cudaStream_t);
 }  // namespace mid
 
 // Lines per tile and threads per CTA of the C5 shapes.
@@ -69,6 +96,19 @@ bool mid_auto(int n, int K) {
     case 512: return mid::auto_ok_n<512>(n);
     case 1024: return n != 1 && n != 9 && mid::auto_ok_n<1024>(n);
     case 2048: return mid::auto_ok_n<2048>(n);
+    case 24: return mid::auto_ok_n<24>(n);
+    case 40: return mid::auto_ok_n<40>(n);
+    case 48: return mid::auto_ok_n<48>(n);
+    case 80: return mid::auto_ok_n<80>(n);
+    case 96: return mid::auto_ok_n<96>(n);
+    case 100: return mid::auto_ok_n<100>(n);
+    case 160: return mid::auto_ok_n<160>(n);
+    case 192: return mid::auto_ok_n<192>(n);
+    case 200: return mid::auto_ok_n<200>(n);
+    case 320: return mid::auto_ok_n<320>(n);
+    case 384: return mid::auto_ok_n<384>(n);
+    case 768: return mid::auto_ok_n<768>(n);
+    case 1000: return mid::auto_ok_n<1000>(n);
     default: return false;
   }
 #else
@@ -118,6 +158,19 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int
       case 512: return mid::launch_auto_n<512>(t, ls, mode, analysis, sym, stream);
       case 1024: return mid::launch_auto_n<1024>(t, ls, mode, analysis, sym, stream);
       case 2048: return mid::launch_auto_n<2048>(t, ls, mode, analysis, sym, stream);
+      case 24: return mid::launch_auto_n<24>(t, ls, mode, analysis, sym, stream);
+      case 40: return mid::launch_auto_n<40>(t, ls, mode, analysis, sym, stream);
+      case 48: return mid::launch_auto_n<48>(t, ls, mode, analysis, sym, stream);
+      case 80: return mid::launch_auto_n<80>(t, ls, mode, analysis, sym, stream);
+      case 96: return mid::launch_auto_n<96>(t, ls, mode, analysis, sym, stream);
+      case 100: return mid::launch_auto_n<100>(t, ls, mode, analysis, sym, stream);
+      case 160: return mid::launch_auto_n<160>(t, ls, mode, analysis, sym, stream);
+      case 192: return mid::launch_auto_n<192>(t, ls, mode, analysis, sym, stream);
+      case 200: return mid::launch_auto_n<200>(t, ls, mode, analysis, sym, stream);
+      case 320: return mid::launch_auto_n<320>(t, ls, mode, analysis, sym, stream);
+      case 384: return mid::launch_auto_n<384>(t, ls, mode, analysis, sym, stream);
+      case 768: return mid::launch_auto_n<768>(t, ls, mode, analysis, sym, stream);
+      case 1000: return mid::launch_auto_n<1000>(t, ls, mode, analysis, sym, stream);
       default: break;
     }
   }

@@ -149,6 +149,104 @@ struct Plan<114, FEW> {
   static constexpr int R[3] = {2, 3, 19};
 };
 
+// Non-power-of-two K (3 * 2^j, 5 * 2^j, 2^i * 5^j): odd radices run as
+// direct DFTs by conjugate pairs (dft_direct).  FEW: radix 16 where it fits.
+template <bool FEW>
+struct Plan<24, FEW> {
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {8, 3};
+};
+template <>
+struct Plan<48, true> {
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {16, 3};
+};
+template <>
+struct Plan<48, false> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 2, 3};
+};
+template <bool FEW>
+struct Plan<96, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 4, 3};
+};
+template <>
+struct Plan<192, true> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {16, 4, 3};
+};
+template <>
+struct Plan<192, false> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 8, 3};
+};
+template <>
+struct Plan<384, true> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {16, 8, 3};
+};
+template <>
+struct Plan<384, false> {
+  static constexpr int NP = 4;
+  static constexpr int R[4] = {8, 8, 2, 3};
+};
+template <>
+struct Plan<768, true> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {16, 16, 3};
+};
+template <>
+struct Plan<768, false> {
+  static constexpr int NP = 4;
+  static constexpr int R[4] = {8, 8, 4, 3};
+};
+template <bool FEW>
+struct Plan<40, FEW> {
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {8, 5};
+};
+template <>
+struct Plan<80, true> {
+  static constexpr int NP = 2;
+  static constexpr int R[2] = {16, 5};
+};
+template <>
+struct Plan<80, false> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 2, 5};
+};
+template <bool FEW>
+struct Plan<160, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 4, 5};
+};
+template <>
+struct Plan<320, true> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {16, 4, 5};
+};
+template <>
+struct Plan<320, false> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 8, 5};
+};
+template <bool FEW>
+struct Plan<100, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {4, 5, 5};
+};
+template <bool FEW>
+struct Plan<200, FEW> {
+  static constexpr int NP = 3;
+  static constexpr int R[3] = {8, 5, 5};
+};
+template <bool FEW>
+struct Plan<1000, FEW> {
+  static constexpr int NP = 4;
+  static constexpr int R[4] = {8, 5, 5, 5};
+};
+
 __device__ __forceinline__ int makhoul_src(int t, int N) { return (2 * t < N) ? 2 * t : 2 * N - 1 - 2 * t; }
 
 // Direct DFT of odd length R (K = 114: R = 19) with roots from the K-point

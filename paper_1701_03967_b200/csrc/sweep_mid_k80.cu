@@ -1,0 +1,9 @@
+// General-shape mid kernels for K = 80, every order (mid::AutoShape); see
+// sweep_mid.cu.  One translation unit per K so the library builds in parallel.
+#include "sweep_mid_impl.cuh"
+
+namespace sfem_b200 {
+namespace mid {
+template cudaError_t launch_auto_n<80>(const DevTable&, const LineSet&, int, int, const SymbolInfo*, cudaStream_t);
+}  // namespace mid
+}  // namespace sfem_b200

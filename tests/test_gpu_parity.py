@@ -299,7 +299,10 @@ def test_long_lines_match_oracle(sfem, n, K):
 MID = [(1, 1024), (2, 512), (4, 256), (9, 114), (9, 1024), (4, 4096),
        # general shapes (mid::AutoShape): every order at K in {16, ..., 512}
        (1, 16), (9, 16), (2, 32), (6, 32), (9, 32), (1, 64), (2, 128), (8, 128), (9, 128),
-       (3, 256), (9, 256), (5, 512), (9, 512), (4, 1024), (8, 1024), (2, 2048), (5, 2048)]
+       (3, 256), (9, 256), (5, 512), (9, 512), (4, 1024), (8, 1024), (2, 2048), (5, 2048),
+       # non-power-of-two K (3 * 2^j, 5 * 2^j, 2^i * 5^j: odd radices 3 and 5)
+       (1, 24), (9, 24), (4, 48), (7, 96), (2, 192), (9, 192), (3, 384), (1, 768), (7, 768),
+       (9, 40), (5, 80), (6, 160), (4, 320), (9, 320), (3, 100), (9, 100), (7, 200), (2, 1000), (9, 1000)]
 
 
 @pytest.mark.parametrize("n,K", MID)
