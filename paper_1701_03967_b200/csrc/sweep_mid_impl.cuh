@@ -352,9 +352,21 @@ __device__ __forceinline__ void fft_pass(double2* W, const double2* __restrict__
 #ifndef SFEM_MID_DIAG_SKIP
 #define SFEM_MID_DIAG_SKIP 0  // diagnostics builds only: 1 skips the FFT passes, 2 the mixes, 3 the fills
 #endif
+// Radix-16 plans where a radix-16 pass keeps one butterfly per thread
+// (SFEM_MID_FEW_RULE = 1: J * N / 16 <= threads, else spills), or with at
+// most 8 jobs per tile (rule 0, the original).
+#ifndef SFEM_MID_FEW_RULE
+#define SFEM_MID_FEW_RULE 0
+#endif
+template <class C>
+__host__ __device__ constexpr bool few_plan() {
+  return SFEM_MID_FEW_RULE ? (C::J * (C::N / 16) <= C::THREADS || C::THREADS >= SFEM_MID_FEW_TH)
+                           : (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH);
+}
+
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
-  using PL = Plan<C::N, (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH)>;
+  using PL = Plan<C::N, few_plan<C>()>;
   if constexpr (P < PL::NP && SFEM_MID_DIAG_SKIP != 1) {
     constexpr int R = PL::R[P];
     fft_pass<C, R, NS>(W, tw);
@@ -410,7 +422,7 @@ __device__ __forceinline__ void fft_pass_oop(const double2* X, double2* Y, const
 // Returns the buffer holding the result.
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ double2* fft_oop(double2* X, double2* Y, const double2* __restrict__ tw) {
-  using PL = Plan<C::N, (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH)>;
+  using PL = Plan<C::N, few_plan<C>()>;
   if constexpr (P < PL::NP) {
     constexpr int R = PL::R[P];
     fft_pass_oop<C, R, NS>(X, Y, tw);
