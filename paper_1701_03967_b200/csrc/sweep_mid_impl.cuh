@@ -419,13 +419,34 @@ __device__ __forceinline__ void fft_pass_oop(const double2* X, double2* Y, const
   __syncthreads();
 }
 
+// Global FFT work slices (sweep_mid_gw): every dead slice is dropped from L2
+// without write-back as soon as a pass has consumed it, so at most one dirty
+// slice per CTA competes for L2.  With both slices only discarded at exit,
+// C2 wrote 3.61 GB to DRAM per launch against 0.54 GB of results
+// (profiles/r1n_ncu_full_c2.json): the 148 x 0.52 MB of work slices were
+// being evicted dirty.
+#ifndef SFEM_MID_GW_DISCARD
+#define SFEM_MID_GW_DISCARD 1
+#endif
+template <class C>
+__device__ __forceinline__ void discard_l2(const double2* W) {
+  constexpr int LINES = (C::J * C::N * 16) / 128;
+  const char* wb = reinterpret_cast<const char*>(W);
+  for (int i = threadIdx.x; i < LINES; i += C::THREADS)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(wb + static_cast<size_t>(i) * 128) : "memory");
+}
+
 // Returns the buffer holding the result.
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ double2* fft_oop(double2* X, double2* Y, const double2* __restrict__ tw) {
   using PL = Plan<C::N, few_plan<C>()>;
   if constexpr (P < PL::NP) {
     constexpr int R = PL::R[P];
-    fft_pass_oop<C, R, NS>(X, Y, tw);
+    fft_pass_oop<C, R, NS>(X, Y, tw);  // ends with a barrier: X is dead
+#if SFEM_MID_GW_DISCARD
+    discard_l2<C>(X);
+    __syncthreads();  // the discards land before the next pass writes X
+#endif
     return fft_oop<C, P + 1, NS * R>(Y, X, tw);
   } else {
     return X;
@@ -1095,14 +1116,21 @@ __global__ void __launch_bounds__(TH, 1)
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
+  const double2* Zf = W0;
   if (MODE != kInverse) {
     forward_fill<C, true>(R, reinterpret_cast<double*>(W0), PS, t.om);
-    const double2* Z = fft_oop<C>(W0, W1, t.tw);
+    Zf = fft_oop<C>(W0, W1, t.tw);
     centre_reduce<C>(PS, C0);
-    forward_post<C, true>(Z, R, t.mk);
+    forward_post<C, true>(Zf, R, t.mk);
   }
   mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
   if (MODE != kForward) {
+#if SFEM_MID_GW_DISCARD
+    if (MODE == kForwardDivideInverse) {  // the forward result is dead (mix ended with a barrier)
+      discard_l2<C>(Zf);
+      __syncthreads();
+    }
+#endif
     inverse_fill<C, true>(R, W0, t.mkh, t.om);
     const double2* Z = fft_oop<C>(W0, W1, t.tw);
     inverse_post<C, true>(Z, R, C0);
