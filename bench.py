@@ -42,9 +42,38 @@ CONFIGS = {
     "c5n4": ([4, 4, 4], [256] * 3, [1.0] * 3, None, 0.5, "3D n=4 K=256 (config 5)"),
     "c5n9": ([9, 9, 9], [114] * 3, [1.0] * 3, None, 0.5, "3D n=9 K=114 (config 5)"),
 }
-# CPU sample for the reference arm / cpu_baseline: same equation, order and
-# dimension, fewer elements (bounded to a few seconds of host work).
-CPU_SAMPLE = {"c4": ([9, 9, 9], [32, 32, 32], [1.0] * 3, 0.0)}
+# config 2: 1-D expansion only (n=4, K=4096, a batch of 4096 lines): FC_n, F_n, F_n^-1
+C2 = (4, 4096, 4096)
+
+
+def ref_sample(cfg_name):
+    """(orders, elements, lengths, shift, same_config) the reference arm solves
+    per step.  A per-axis coefficient a_i is the reference's lengths X_i/sqrt(a_i)
+    (solve_with_load uses the lengths only through 4/h_i^2)."""
+    orders, elements, lengths, coeffs, shift, _ = CONFIGS[cfg_name]
+    lengths = [X / (a ** 0.5) for X, a in zip(lengths, coeffs or [1.0] * len(lengths))]
+    elements = list(elements)
+    same = True
+    while np.prod([n * K - 1 for n, K in zip(orders, elements)]) > REF_MAX_UNKNOWNS:
+        elements = [max(2, K // 2) for K in elements]
+        same = False
+    return orders, elements, lengths, shift, same
+
+
+def ref_sample_text(orders, elements, U, same):
+    ext = "x".join(str(n * K - 1) for n, K in zip(orders, elements))
+    return (f"{len(orders)}D n={orders[0]} K={elements[0]} ({ext} = {U} unknowns"
+            f"{', the same configuration' if same else ', a smaller-K sample of the configuration'}), "
+            "the reference's solve_with_load (algorithm (a)) with its own seconds_solve timer, median over the "
+            "timed solves after a warm-up solve; FFTW (absent from the image) replaced by the oracle/shim FFT")
+
+# The reference arm and cpu_baseline run the reference's own solver on the
+# SAME configuration when one solve fits a few seconds of host work (C1, C3,
+# C4: <= 2.5e8 unknowns); the 1.07e9-unknown C5 shapes are sampled with
+# fewer elements per axis (same orders and equation; same_config false).
+REF_MAX_UNKNOWNS = 2.5e8
+# Configs timed device-resident beside the headline (the "configs" object).
+SIDE_CONFIGS = ["c1", "c2", "c3", "c5n1", "c5n2", "c5n4", "c5n9"]
 
 METRIC = "FP64 FEM unknowns solved/sec (3D n=9) and achieved HBM GB/s vs roofline"
 
@@ -138,19 +167,90 @@ def barrier(dist, world):
         dist.barrier()
 
 
-def cpu_reference_sample(cfg_name, reps=1):
-    """The reference's own solver (oracle/_ref) on the bounded CPU sample."""
+def cpu_reference_sample(cfg_name, reps=5, warmup=1):
+    """The reference's own solver (oracle/_ref) on the arm's workload: `warmup`
+    untimed solves, then `reps` solves, each timed by the reference's own
+    seconds_solve (poisson.cpp:781-785); the acceptance suite's median of 5
+    after a warm-up (acceptance_main.cpp:264-273)."""
     from oracle import reflib
-    orders, elements, lengths, shift = CPU_SAMPLE[cfg_name]
+    orders, elements, lengths, shift, same = ref_sample(cfg_name)
     ext = [n * K - 1 for n, K in zip(orders, elements)]
     f = np.random.default_rng(0).uniform(-1.0, 1.0, ext)
-    reflib.solve(f, orders, elements, lengths, shift)  # tables + page-in, untimed
-    secs = []
-    for _ in range(reps):
-        _, s = reflib.solve(f, orders, elements, lengths, shift)
-        secs.append(s)
+    secs = reflib.solve_repeat(f, orders, elements, lengths, shift, warmup + reps)[warmup:]
     U = int(np.prod(ext))
-    return U, secs, reflib.max_threads(), f"3D n={orders[0]} K={elements[0]} ({'x'.join(map(str, ext))} = {U} unknowns), solve_with_load seconds_solve"
+    return U, secs, reflib.max_threads(), ref_sample_text(orders, elements, U, same), same
+
+
+def side_configs(sfem, ctx, args):
+    """Device-resident times of the other BASELINE configs in the same run and
+    clocks: a few warm-up solves, then `reps` solves bracketed by CUDA events
+    on the plan stream; frac = algorithmic bytes (16 B per unknown per sweep
+    launch) / time / measured HBM peak.  Loads are seeded U[-1,1] drawn on the
+    device (values do not change the work)."""
+    import torch
+    peaks, _ = measured_peaks()
+    out = {}
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    gen = torch.Generator(device="cuda")
+    for name in SIDE_CONFIGS:
+        try:
+            if name == "c2":
+                n, K, count = C2
+                t = sfem.SpectralTable(n, K, ctx)
+                L = n * K - 1
+                gen.manual_seed(0)
+                x = torch.randn(count, L, dtype=torch.float64, device="cuda", generator=gen)
+                y = torch.empty_like(x)
+                ms = {}
+                for op, label in ((sfem.DECOMPOSE_WEIGHTED, "fc_n"), (sfem.DECOMPOSE, "f_n"),
+                                  (sfem.SYNTHESIZE, "f_n_inverse")):
+                    for _ in range(3):
+                        sfem.lines_device(t, op, count, x.data_ptr(), L, y.data_ptr(), L, ctx.stream)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    torch.cuda.synchronize()
+                    reps = 10
+                    e0.record(stream)
+                    for _ in range(reps):
+                        sfem.lines_device(t, op, count, x.data_ptr(), L, y.data_ptr(), L, ctx.stream)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms[label] = e0.elapsed_time(e1) / reps
+                worst = max(ms.values())
+                out[name] = {"workload": "1D n=4 K=4096, 4096 lines (config 2)", "values": count * L,
+                             "ms_per_op": {k: round(v, 4) for k, v in ms.items()},
+                             "frac": 16.0 * count * L / (worst * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                             "frac_note": "slowest of the three ops; 16 B per value per op"}
+                del x, y, t
+                torch.cuda.empty_cache()
+                continue
+            orders, elements, lengths, coeffs, shift, desc = CONFIGS[name]
+            spec = sfem.ProblemSpec(len(orders), lengths, elements, orders, shift, coefficients=coeffs)
+            plan = sfem.Plan(spec, ctx)
+            rows = plan.unknowns // plan.extents[-1]
+            gen.manual_seed(0)
+            buf = torch.rand(rows, plan.pitch, dtype=torch.float64, device="cuda", generator=gen)
+            buf.mul_(2.0).sub_(1.0)
+            reps = 5 if plan.unknowns > 5e8 else 20
+            for _ in range(3):
+                plan.solve_device(buf.data_ptr())
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                plan.solve_device(buf.data_ptr())
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            _, kern = plan.solve_device_timed(buf.data_ptr(), reps=2)
+            out[name] = {"workload": desc, "unknowns": plan.unknowns, "ms": round(ms, 4),
+                         "unknowns_per_s": plan.unknowns / (ms * 1e-3),
+                         "kernel_ms": [round(v, 4) for v in kern],
+                         "frac": 16.0 * plan.unknowns * plan.launches / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+            del buf, plan
+            torch.cuda.empty_cache()
+        except Exception as e:  # reported, not fatal
+            out[name] = {"error": repr(e)}
+    return out
 
 
 def run_reference(args, world, rank):
@@ -159,26 +259,20 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     from oracle import reflib
-    orders, elements, lengths, shift = CPU_SAMPLE[args.config]
-    ext = [n * K - 1 for n, K in zip(orders, elements)]
-    U = int(np.prod(ext))
-    f = np.random.default_rng(0).uniform(-1.0, 1.0, ext)
-    for _ in range(args.warmup):
-        reflib.solve(f, orders, elements, lengths, shift)
-    secs = []
-    for _ in range(args.steps):
-        _, s = reflib.solve(f, orders, elements, lengths, shift)
-        secs.append(s)
-    t = float(sum(secs))
-    value = U * args.steps / t
-    sample = (f"3D n={orders[0]} K={elements[0]} ({U} unknowns) per step, the reference's solve_with_load "
-              f"(algorithm (a)) with its own seconds_solve timer; FFTW replaced by the oracle/shim FFT")
+    if not reflib.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsfem_ref.so not built"}), flush=True)
+        return
+    U, secs, cores, sample, same = cpu_reference_sample(args.config, reps=args.steps, warmup=args.warmup)
+    med = statistics.median(secs)
+    value = U / med
     line = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "unknowns/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * med,
+        "ms_per_step_mean": 1e3 * float(np.mean(secs)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][5], "cpu_sample": sample, "parallelism": "openmp"},
-        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": reflib.max_threads(), "kind": "reference",
+        "config": {"workload": CONFIGS[args.config][5], "cpu_sample": sample, "same_config": same,
+                   "parallelism": f"openmp x{cores}"},
+        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -225,18 +319,25 @@ def run_peer(args, world, rank, local, dist):
         # global load on rank 0 (rank 0's slab depends on every rank's rows
         # through the two exchanges): a fused exchange that moved the wrong
         # data is reported and the NCCL path takes over, never timed as is.
-        solve()
-        torch.cuda.synchronize()
-        mine = plan.gather_x()
+        # Any local failure (a barrier that timed out, an exception) becomes
+        # err = inf in the one all-reduce every rank reaches.
         err = 0.0
-        if rank == 0:
-            offs, lens = D.partition_even(plan.extents[0], world)
-            glob = np.concatenate([np.random.default_rng(1000 + r).uniform(-1.0, 1.0, (lens[r], L1, L2))
-                                   for r in range(world)])
-            want, _ = sfem.solve_dof(spec, glob, ctx=ctx)
-            want = want[offs[0]:offs[0] + lens[0]]
-            err = float(np.linalg.norm(mine - want) / np.linalg.norm(want))
-            del glob, want
+        try:
+            solve()
+            if plan.barrier_timeout(ctx.stream):
+                raise RuntimeError("device barrier timed out waiting for a peer")
+            mine = plan.gather_x()
+            if rank == 0:
+                offs, lens = D.partition_even(plan.extents[0], world)
+                glob = np.concatenate([np.random.default_rng(1000 + r).uniform(-1.0, 1.0, (lens[r], L1, L2))
+                                       for r in range(world)])
+                want, _ = sfem.solve_dof(spec, glob, ctx=ctx)
+                want = want[offs[0]:offs[0] + lens[0]]
+                err = float(np.linalg.norm(mine - want) / np.linalg.norm(want))
+                del glob, want
+        except Exception as e:
+            print(f"[bench] rank {rank}: fused NVLink check failed locally: {e!r}", file=sys.stderr)
+            err = float("inf")
         err = max_over_ranks(err, dist, world)
         if not err <= 1e-11:
             raise RuntimeError(f"fused NVLink solve differs from the single-GPU solve (rank-0 slab rel-L2 {err:.3e})")
@@ -261,7 +362,12 @@ def run_peer(args, world, rank, local, dist):
         ev1.record(ext)
         torch.cuda.synchronize()
     barrier(dist, world)
-    ms = max_over_ranks(ev0.elapsed_time(ev1), dist, world)
+    ms = ev0.elapsed_time(ev1)
+    if plan.barrier_timeout(ctx.stream):  # a timed-out barrier: the timed solves are not valid
+        ms = float("inf")
+    ms = max_over_ranks(ms, dist, world)
+    if ms == float("inf"):
+        raise RuntimeError("a device barrier timed out during the timed solves")
     value = U * args.steps / (ms * 1e-3)
     ms_step = ms / args.steps
     peaks, peak_kind = measured_peaks()
@@ -400,6 +506,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the device-timed side configs (C1, C2, C3, C5)")
     ap.add_argument("--no-verify", action="store_true",
                     help="N > 1: skip the set-up check of the fused exchange against a single-GPU solve")
     ap.add_argument("--dist-mode", default="peer", choices=["peer", "nccl"],
@@ -443,7 +550,7 @@ def main():
             ok = False
             print(f"[bench] fused NVLink solve failed on rank {rank}: {e!r}; NCCL slab path next", file=sys.stderr)
             args.dist_error = repr(e)
-        flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+        flag = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if flag.item() == 1.0:
             dist.destroy_process_group()
@@ -542,14 +649,20 @@ def main():
            "ms_per_step": e2e_s * 1e3, "steps": n_e2e, "api": "sfem_cuda_solve_host_batch (pinned host buffers)",
            "single_solve_latency_ms": lat_s * 1e3}
 
+    side = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        del buf
+        torch.cuda.empty_cache()
+        side = side_configs(sfem, ctx, args)
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and args.config in CPU_SAMPLE:
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
             from oracle import reflib
             if reflib.available():
-                Us, secs, cores, sample = cpu_reference_sample(args.config, reps=2)
-                cpu = {"value": Us / min(secs), "unit": "unknowns/s", "cores": cores, "kind": "reference",
-                       "sample": sample + "; FFTW replaced by the oracle/shim FFT"}
+                Us, secs, cores, sample, same = cpu_reference_sample(args.config, reps=5, warmup=1)
+                cpu = {"value": Us / statistics.median(secs), "unit": "unknowns/s", "cores": cores,
+                       "kind": "reference", "sample": sample, "same_config": same}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "unknowns/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -569,6 +682,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "configs": side,
             "gpu_launches": plan.launches * args.steps,
             "clocks": clk.summary(),
         }

@@ -136,7 +136,13 @@ int sfem_cuda_plan_set_algorithm(sfem_plan plan, int algorithm);
 /* Device-resident solve, in place: d_data holds the load (dof layout, last
  * axis padded to `pitch` elements) and receives u.  Replaces
  * solve_with_load's timed core run_full_diagonalization (poisson.cpp:637-669,
- * timed region 781-785).  stream NULL = the context stream. */
+ * timed region 781-785).  stream NULL = the context stream.  Any pitch >=
+ * L_{N-1} may be passed per call (the plan's own buffers keep their size).
+ * Plan-owned scratch is shared by all of the plan's solves: a solve issued on
+ * a different stream than the previous one is ordered after it (event wait),
+ * so one plan never runs two solves concurrently; use one plan per stream for
+ * concurrent solves.  The same holds for a context's global FFT scratch
+ * across its plans and line calls. */
 int sfem_cuda_solve_device(sfem_plan plan, double* d_data, long long pitch, void* stream);
 
 /* Host solve: dense dof-layout load in, dense u out (h_u may equal h_load).
@@ -254,6 +260,11 @@ int sfem_cuda_peer_buffers(sfem_peer peer, void** x_slab, void** y_slab, void** 
  * (all ranks on one device, phases run rank after rank: the loopback check). */
 int sfem_cuda_peer_bind(sfem_peer peer, void* const* x_slabs, void* const* y_slabs, void* const* flags);
 int sfem_cuda_peer_phase(sfem_peer peer, int phase, void* stream);
+/* After synchronising `stream` (NULL = context stream): the epoch of a device
+ * barrier that gave up after 20 s because a peer never arrived (0 = none).
+ * A barrier that times out returns instead of trapping, so the context stays
+ * usable and every rank can agree on a fallback. */
+int sfem_cuda_peer_status(sfem_peer peer, void* stream, long long* timed_out_epoch);
 /* CUDA IPC of a device allocation between the ranks' processes (64-byte handles). */
 int sfem_cuda_ipc_get_handle(void* d_ptr, void* handle);
 int sfem_cuda_ipc_open_handle(const void* handle, void** d_ptr);

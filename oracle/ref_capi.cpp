@@ -344,6 +344,23 @@ int sfemref_solve(int dim, const int* orders, const int* elements, const double*
   });
 }
 
+// `reps` timed solve_with_load calls of one load (the bench's CPU legs): the
+// dof -> class conversion is done once, each call's own seconds_solve
+// (poisson.cpp:781-785) lands in seconds[i]; the tables are built untimed by
+// the first call (poisson.cpp:776-779), as in every reference solve.
+int sfemref_solve_repeat(int dim, const int* orders, const int* elements, const double* lengths, double shift,
+                         int threads, int reps, const double* load_dof, double* seconds) {
+  return guarded([&] {
+    const ProblemSpec spec = make_spec(dim, orders, elements, lengths, shift);
+    spec.validate();
+    const GridFunctionND load = grid_from_dof(spec.axis_specs(), load_dof);
+    SolveOptions opt;
+    opt.algorithm = Algorithm::FullDiagonalization;
+    opt.threads = threads;
+    for (int r = 0; r < reps; ++r) seconds[r] = solve_with_load(spec, load, tables(), opt).seconds_solve;
+  });
+}
+
 // Operator apply (poisson.cpp:749-769) on dof-layout data (verification only).
 int sfemref_apply_operator(int dim, const int* orders, const int* elements, const double* lengths,
                            double shift, const double* v_dof, double* out_dof) {

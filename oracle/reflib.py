@@ -41,6 +41,8 @@ def lib():
         L.sfemref_lines.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, _dp, _dp]
         L.sfemref_solve.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                     _dp, _dp, _dp]
+        L.sfemref_solve_repeat.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                           _dp, _dp]
         L.sfemref_apply_operator.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, _dp, _dp]
         L.sfemref_fem_load_sines.argtypes = [ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, _dp, _dp]
         L.sfemref_fem_load_case.argtypes = [ctypes.c_char_p, ctypes.c_int, _ip, _ip, _dp, ctypes.c_double, _dp]
@@ -160,6 +162,16 @@ def solve(load: np.ndarray, orders, elements, lengths, shift, algorithm=0, threa
                              _p(np.array(lengths, float)), float(shift), algorithm, threads, _p(load), _p(u),
                              _p(sec)))
     return u, float(sec[0])
+
+
+def solve_repeat(load: np.ndarray, orders, elements, lengths, shift, reps: int, threads=0):
+    """`reps` solve_with_load calls of one load; each call's seconds_solve."""
+    load = np.ascontiguousarray(load, float)
+    N = load.ndim
+    sec = np.zeros(reps)
+    _chk(lib().sfemref_solve_repeat(N, (ctypes.c_int * N)(*orders), (ctypes.c_int * N)(*elements),
+                                    _p(np.array(lengths, float)), float(shift), threads, reps, _p(load), _p(sec)))
+    return [float(x) for x in sec]
 
 
 def apply_operator(v: np.ndarray, orders, elements, lengths, shift):

@@ -118,6 +118,7 @@ _SIGS = [
     ("sfem_cuda_peer_buffers", ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     ("sfem_cuda_peer_bind", ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     ("sfem_cuda_peer_phase", ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+    ("sfem_cuda_peer_status", ctypes.c_int, [_vp, _vp, _llp]),
     ("sfem_cuda_ipc_get_handle", ctypes.c_int, [_vp, _vp]),
     ("sfem_cuda_ipc_open_handle", ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     ("sfem_cuda_ipc_close", ctypes.c_int, [_vp]),

@@ -100,6 +100,12 @@ struct sfem_ctx_s {
   cudaStream_t stream = nullptr;
   double* scratch = nullptr;
   size_t scratch_doubles = 0;
+  // The scratch is shared by every plan and lines call of the context, each
+  // on the caller's stream: the last user's stream and an event after its
+  // launch order a user on another stream behind it (scratch_for/scratch_done).
+  cudaEvent_t scratch_ev = nullptr;
+  cudaStream_t scratch_stream = nullptr;
+  bool scratch_pending = false;
   TableCache table_cache;  // TableSet's cache directory (poisson.cpp:49-73); empty = none
 };
 
@@ -244,19 +250,32 @@ void encode_smap(Step& s, const double* data) {
 
 }  // namespace
 
-// Per-context scratch for global-work sweeps (grown on demand).
-static double* scratch_for(sfem_ctx ctx, size_t doubles) {
+// Per-context scratch for global-work sweeps (grown on demand).  A caller on
+// `stream` waits for the previous user's launch if that ran on another stream;
+// growing it synchronises the device (the old buffer may be in use anywhere).
+static double* scratch_for(sfem_ctx ctx, size_t doubles, cudaStream_t stream) {
   if (doubles > ctx->scratch_doubles) {
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (ctx->scratch) {
-      ck(cudaStreamSynchronize(ctx->stream), "sync");
+      ck(cudaDeviceSynchronize(), "sync");
       ck(cudaFree(ctx->scratch), "cudaFree(scratch)");
     }
     ctx->scratch = nullptr;
+    ctx->scratch_pending = false;
     ck(cudaMalloc(&ctx->scratch, doubles * sizeof(double)), "cudaMalloc(scratch)");
     ctx->scratch_doubles = doubles;
   }
+  if (!ctx->scratch_ev) ck(cudaEventCreateWithFlags(&ctx->scratch_ev, cudaEventDisableTiming), "event");
+  if (ctx->scratch_pending && ctx->scratch_stream != stream)
+    ck(cudaStreamWaitEvent(stream, ctx->scratch_ev, 0), "scratch: wait for the previous user");
   return ctx->scratch;
+}
+
+// After a launch that used the scratch on `stream`.
+static void scratch_done(sfem_ctx ctx, cudaStream_t stream) {
+  ck(cudaEventRecord(ctx->scratch_ev, stream), "event");
+  ctx->scratch_stream = stream;
+  ctx->scratch_pending = true;
 }
 
 namespace {
@@ -410,12 +429,14 @@ void launch_steps(std::vector<Step>& steps, double* user, sfem_ctx ctx, cudaStre
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
     } else if (s.use_fast && has_mid_sweep(dt.n, dt.K)) {
       const size_t wd = mid_work_doubles(dt.n, dt.K, s.ls.nlines);
-      double* gw = wd ? scratch_for(ctx, wd) : nullptr;
+      double* gw = wd ? scratch_for(ctx, wd, stream) : nullptr;
       ck(launch_sweep_mid(dt, s.ls, s.mode, kWeighted, sym, stream, gw), "mid sweep launch");
+      if (gw) scratch_done(ctx, stream);
     } else {
       double* gw = nullptr;
-      if (s.gwork) gw = scratch_for(ctx, sweep_work_doubles(dt, s.B) * ((s.ls.nlines + s.B - 1) / s.B));
+      if (s.gwork) gw = scratch_for(ctx, sweep_work_doubles(dt, s.B) * ((s.ls.nlines + s.B - 1) / s.B), stream);
       ck(launch_sweep(dt, s.ls, s.mode, kWeighted, sym, s.B, stream, gw), "sweep launch");
+      if (gw) scratch_done(ctx, stream);
     }
   }
   if (kev) ck(cudaEventRecord((*kev)[steps.size()], stream), "event");
@@ -432,18 +453,25 @@ struct sfem_plan_s {
   std::vector<std::unique_ptr<sfem_table_s>> owned;
   std::vector<sfem_table_s*> tables;  // per axis
   std::vector<long long> ext;
-  long long pitch = 0;
+  long long pitch = 0;        // the plan's own padded pitch (fixed at creation; sizes dwork / fbuf / dstage)
+  long long steps_pitch = 0;  // the caller pitch `steps` were last built for
   long long rows = 0;  // product of leading extents
   std::vector<Step> steps;
   int algorithm = 0;            // 0: full diagonalisation (a), 1: partial (b)
   std::vector<Step> pfwd, pinv; // algorithm (b): forward / inverse sweeps of axes N-1 .. 1
   BandArgs band{};              // algorithm (b): the axis-0 line solves
   double* cbuf = nullptr;       // their Thomas coefficients
+  size_t cbuf_cap = 0;          // doubles allocated in cbuf
   unsigned long long* dfail = nullptr;
   unsigned long long* hfail = nullptr;  // pinned copy of the failure flag
   bool blocked = false;         // 3-D blocked schedule (build_blocked_steps)
   double* bwork = nullptr;      // its scratch tensor [x_hi][L1][x_lo][bpitch]
   size_t belems = 0;
+  size_t bwork_cap = 0;         // doubles allocated in bwork
+  // plan-owned scratch (bwork, cbuf) is shared by solves on any stream: a
+  // solve on another stream than the previous one waits for it
+  cudaEvent_t busy_ev = nullptr;
+  cudaStream_t busy_stream = nullptr;
   long long bpitch = 0;
   double* dwork = nullptr;
   double* dstage = nullptr;  // dense host-transfer staging
@@ -459,6 +487,7 @@ struct sfem_plan_s {
   bool use_fast = true;
   // operator / residual scratch (P and Q tensors, padded) and reduction slots
   double* opwork[2] = {nullptr, nullptr};
+  size_t opwork_cap[2] = {0, 0};  // doubles allocated per operator scratch tensor
   unsigned long long* dred = nullptr;
   double* fbuf = nullptr;      // device load of sfem_cuda_solve_field / operator output
   double* load_vec = nullptr;  // per-axis 1-D loads of separable fields
@@ -657,11 +686,28 @@ void build_partial_steps(sfem_plan_s* p, long long pitch) {
   }
 }
 
+// Grow a device buffer to at least `need` doubles (contents not kept).  The
+// old buffer may still be read by work queued on `stream` or another stream,
+// so the device is synchronised before it is freed (cold path: first use or a
+// larger caller pitch).
+void ensure_capacity(double*& buf, size_t& cap, size_t need, const char* what) {
+  if (buf && cap >= need) return;
+  if (buf) {
+    ck(cudaDeviceSynchronize(), "sync before realloc");
+    ck(cudaFree(buf), "cudaFree");
+    buf = nullptr;
+    cap = 0;
+  }
+  ck(cudaMalloc(&buf, std::max<size_t>(need, 1) * sizeof(double)), what);
+  cap = need;
+}
+
 void run_partial(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream) {
   if (pitch != p->band.pitch || p->pfwd.empty()) build_partial_steps(p, pitch);
   const size_t lines = static_cast<size_t>(p->band.inner * p->band.outer);
-  if (!p->cbuf) {
-    ck(cudaMalloc(&p->cbuf, static_cast<size_t>(p->band.K) * lines * sizeof(double)), "cudaMalloc(band scratch)");
+  // the line count includes the caller's pitch: grow the coefficient scratch with it
+  ensure_capacity(p->cbuf, p->cbuf_cap, static_cast<size_t>(p->band.K) * lines, "cudaMalloc(band scratch)");
+  if (!p->dfail) {
     ck(cudaMalloc(&p->dfail, sizeof(unsigned long long)), "cudaMalloc(flag)");
     ck(cudaMallocHost(&p->hfail, sizeof(unsigned long long)), "cudaMallocHost(flag)");
   }
@@ -695,17 +741,28 @@ void check_partial(const sfem_plan_s* p) {
        std::to_string(sigma) + "); shift too negative");
 }
 
-void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
+void run_steps_impl(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
   if (p->algorithm == 1) {
     run_partial(p, data, pitch, stream);
     return;
   }
-  if (pitch != p->pitch) build_steps(p, pitch), p->pitch = pitch;
-  if (p->blocked && !p->bwork) {
-    ck(cudaMalloc(&p->bwork, p->belems * sizeof(double)), "cudaMalloc(blocked scratch)");
+  // Steps are rebuilt for a new caller pitch; p->pitch (the plan's own
+  // padded pitch, which sizes dwork / fbuf / dstage) never changes.
+  if (pitch != p->steps_pitch) build_steps(p, pitch), p->steps_pitch = pitch;
+  if (p->blocked && p->bwork_cap < p->belems) {
+    ensure_capacity(p->bwork, p->bwork_cap, p->belems, "cudaMalloc(blocked scratch)");
     ck(cudaMemsetAsync(p->bwork, 0, p->belems * sizeof(double), stream), "memset(blocked scratch)");
   }
   launch_steps(p->steps, data, p->ctx, stream, events ? &p->kev : nullptr, p->bwork);
+}
+
+void run_steps(sfem_plan_s* p, double* data, long long pitch, cudaStream_t stream, bool events) {
+  if (!p->busy_ev) ck(cudaEventCreateWithFlags(&p->busy_ev, cudaEventDisableTiming), "event");
+  if (p->busy_stream && p->busy_stream != stream)
+    ck(cudaStreamWaitEvent(stream, p->busy_ev, 0), "plan: wait for the previous solve");
+  run_steps_impl(p, data, pitch, stream, events);
+  ck(cudaEventRecord(p->busy_ev, stream), "event");
+  p->busy_stream = stream;
 }
 
 // Reference ProblemSpec::validate (poisson.cpp:32-47), with per-axis coefficients.
@@ -979,8 +1036,7 @@ void apply_sweeps(sfem_plan_s* p, const double* v, double* q_out, const double* 
                   cudaStream_t s) {
   const size_t elems = padded_elems(p, pitch);
   const int nbuf = f ? 2 : 1;
-  for (int b = 0; b < nbuf; ++b)
-    if (!p->opwork[b]) ck(cudaMalloc(&p->opwork[b], elems * sizeof(double)), "cudaMalloc(operator scratch)");
+  for (int b = 0; b < nbuf; ++b) ensure_capacity(p->opwork[b], p->opwork_cap[b], elems, "cudaMalloc(operator scratch)");
   double* P = p->opwork[0];
   double* Q = f ? p->opwork[1] : q_out;
   const std::vector<long long> st = dof_strides(p, pitch);
@@ -1095,6 +1151,7 @@ int sfem_cuda_ctx_destroy(sfem_ctx ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->scratch_ev) cudaEventDestroy(ctx->scratch_ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -1281,13 +1338,15 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
       ck(launch_sweep_fast(t->dev, ls, mode, analysis, nullptr, s), "lines launch (fast)");
     } else if (fast_enabled() && has_mid_sweep(t->dev.n, t->dev.K)) {
       const size_t wd = mid_work_doubles(t->dev.n, t->dev.K, count);
-      double* gw = wd ? scratch_for(t->ctx, wd) : nullptr;
+      double* gw = wd ? scratch_for(t->ctx, wd, s) : nullptr;
       ck(launch_sweep_mid(t->dev, ls, mode, analysis, nullptr, s, gw), "lines launch (mid)");
+      if (gw) scratch_done(t->ctx, s);
     } else {
       bool gwork = false;
       const int B = choose_tile(t->dev, count, &gwork);
-      double* gw = gwork ? scratch_for(t->ctx, sweep_work_doubles(t->dev, B) * ((count + B - 1) / B)) : nullptr;
+      double* gw = gwork ? scratch_for(t->ctx, sweep_work_doubles(t->dev, B) * ((count + B - 1) / B), s) : nullptr;
       ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s, gw), "lines launch");
+      if (gw) scratch_done(t->ctx, s);
     }
   });
 }
@@ -1352,6 +1411,7 @@ int sfem_cuda_plan_create(sfem_ctx ctx, int dim, const int* orders, const int* e
     const long long last = p->ext[dim - 1];
     p->pitch = (last + 3) & ~3LL;  // 32-byte rows
     build_steps(p.get(), p->pitch);
+    p->steps_pitch = p->pitch;
     ck(cudaEventCreate(&p->ev[0]), "event");
     ck(cudaEventCreate(&p->ev[1]), "event");
     p->kev.resize(p->steps.size() + 1);
@@ -1366,6 +1426,7 @@ int sfem_cuda_plan_destroy(sfem_plan p) {
     cudaSetDevice(p->ctx->device);
     if (p->dwork) cudaFree(p->dwork);
     if (p->bwork) cudaFree(p->bwork);
+    if (p->busy_ev) cudaEventDestroy(p->busy_ev);
     if (p->cbuf) cudaFree(p->cbuf);
     if (p->dfail) cudaFree(p->dfail);
     if (p->hfail) cudaFreeHost(p->hfail);
@@ -1952,10 +2013,12 @@ int sfem_cuda_peer_create(sfem_ctx ctx, int dim, const int* orders, const int* e
     ck(cudaSetDevice(ctx->device), "cudaSetDevice");
     ck(cudaMalloc(&d->xbuf, d->x_elems * sizeof(double)), "cudaMalloc(x-slab)");
     ck(cudaMalloc(&d->ybuf, d->y_elems * sizeof(double)), "cudaMalloc(y-slab)");
-    ck(cudaMalloc(&d->flags, kMaxPeer * sizeof(unsigned long long)), "cudaMalloc(flags)");
+    // kMaxPeer arrival words (written by the peers) + this rank's timeout word
+    ck(cudaMalloc(&d->flags, (kMaxPeer + 1) * sizeof(unsigned long long)), "cudaMalloc(flags)");
     ck(cudaMemset(d->xbuf, 0, d->x_elems * sizeof(double)), "memset");
     ck(cudaMemset(d->ybuf, 0, d->y_elems * sizeof(double)), "memset");
-    ck(cudaMemset(d->flags, 0, kMaxPeer * sizeof(unsigned long long)), "memset");
+    ck(cudaMemset(d->flags, 0, (kMaxPeer + 1) * sizeof(unsigned long long)), "memset");
+    d->pf.timeout = d->flags + kMaxPeer;
     *out = d.release();
   });
 }
@@ -2063,6 +2126,18 @@ int sfem_cuda_peer_phase(sfem_peer d, int phase, void* stream) {
       default:
         fail("peer_phase: unknown phase");
     }
+  });
+}
+
+int sfem_cuda_peer_status(sfem_peer d, void* stream, long long* timed_out_epoch) {
+  return guarded([&] {
+    require(d && timed_out_epoch, "peer_status: null argument");
+    ck(cudaSetDevice(d->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    ck(cudaStreamSynchronize(s), "peer_status: sync");
+    unsigned long long v = 0;
+    ck(cudaMemcpy(&v, d->pf.timeout, sizeof v, cudaMemcpyDeviceToHost), "peer_status: read");
+    *timed_out_epoch = static_cast<long long>(v);
   });
 }
 

@@ -137,6 +137,7 @@ cudaError_t launch_sweep_tma_scatter(const DevTable& t, const void* tmap, const 
 // flags[rank][0..nranks) all reach `epoch` (system-scope release / acquire).
 struct PeerFlags {
   unsigned long long* f[kMaxPeer];
+  unsigned long long* timeout;  // this rank's word: epoch of a barrier that timed out (0 = none)
 };
 cudaError_t launch_peer_barrier(const PeerFlags& fl, int nranks, int rank, unsigned long long epoch,
                                 cudaStream_t stream);

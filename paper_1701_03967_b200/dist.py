@@ -249,6 +249,13 @@ class PeerPlan:
     def phase(self, ph: int, stream: int = 0):
         _check(lib.sfem_cuda_peer_phase(self.handle, ph, _vp(stream or None)))
 
+    def barrier_timeout(self, stream: int = 0) -> int:
+        """Synchronise `stream`; the epoch of a device barrier that gave up
+        waiting for a peer (0 = every barrier completed)."""
+        v = ctypes.c_longlong()
+        _check(lib.sfem_cuda_peer_status(self.handle, _vp(stream or None), ctypes.byref(v)))
+        return v.value
+
     def solve(self, stream: int = 0):
         """One solve (the bound ranks run their phases concurrently on their
         own devices; the device barriers order the exchanges)."""

@@ -275,7 +275,7 @@ def test_config3_full_size_matches_reference(sfem):
 
 @needs_ref
 @pytest.mark.slow
-@pytest.mark.parametrize("n,K", [(4, 256), (9, 114)])
+@pytest.mark.parametrize("n,K", [(1, 1024), (2, 512), (4, 256), (9, 114)])
 def test_config5_full_size_matches_reference(sfem, n, K):
     # C5: 3D, nK ~ 1024 per axis (~1.07e9 unknowns, 8.6 GB per FP64 array),
     # -Laplace u + 0.5 u = f, f ~ U[-1,1]
@@ -390,3 +390,63 @@ def test_partial_diagonalization_config4_full_size(sfem):
     err_ours, err_ref = rel_l2(u, ref_a), rel_l2(ref_b, ref_a)
     assert err_ours <= 1e-11 and err_ours <= err_ref
     assert rel_l2(u, ref_b) <= 2 * err_ref + 1e-12
+
+
+def _solve_dev_pitched(sfem, plan, f, pitch, stream=0):
+    import torch
+    lead = f.shape[:-1]
+    buf = torch.zeros(lead + (pitch,), dtype=torch.float64, device="cuda")
+    buf[..., :f.shape[-1]] = torch.from_numpy(f)
+    plan.solve_device(buf.data_ptr(), pitch, stream)
+    torch.cuda.synchronize()
+    return buf[..., :f.shape[-1]].cpu().numpy()
+
+
+@pytest.mark.parametrize("orders,elements", [([3, 2, 3], [8, 5, 8]), ([9, 9, 9], [4, 4, 4]), ([2, 3], [9, 7])])
+def test_caller_pitch_then_plan_buffers(sfem, orders, elements):
+    # a solve_device with the unpadded pitch (= last extent) or a
+    # larger one must not change the buffers the host entry points size from
+    # the plan pitch (solve_host, solve_field, apply_operator_host, algorithm (b)).
+    N = len(orders)
+    spec = sfem.ProblemSpec(N, [1.0] * N, elements, orders, 0.5)
+    plan = sfem.Plan(spec)
+    f = np.random.default_rng(3).uniform(-1, 1, spec.extents())
+    want = O.solve_full_diagonalization(f, orders, elements, [1.0] * N, 0.5)
+    last = spec.extents()[-1]
+    for pitch in (last, plan.pitch + 8, last):
+        u = _solve_dev_pitched(sfem, plan, f, pitch)
+        assert rel_l2(u, want) <= TOL, pitch
+        u2, _ = plan.solve_host(f)
+        assert rel_l2(u2, want) <= TOL, pitch
+        y = plan.apply_operator_host(u2)
+        assert rel_l2(y, f) <= 1e-9, pitch
+        rep = plan.solve_field(sfem.Field.constant(1.0), compute_residual=True)
+        assert rep.residual_rel < 1e-9
+    plan.set_algorithm("partial")
+    for pitch in (plan.pitch + 12, last):
+        u = _solve_dev_pitched(sfem, plan, f, pitch)
+        assert rel_l2(u, want) <= 1e-10, pitch
+    u2, _ = plan.solve_host(f)
+    assert rel_l2(u2, want) <= 1e-10
+
+
+def test_plan_on_two_streams_is_ordered(sfem):
+    # a plan's scratch (blocked schedule) shared by solves on two streams
+    import torch
+    spec = sfem.ProblemSpec(3, [1.0] * 3, [64, 64, 64], [2, 2, 2], 0.0)
+    plan = sfem.Plan(spec)
+    rng = np.random.default_rng(4)
+    fs = [rng.uniform(-1, 1, spec.extents()) for _ in range(4)]
+    wants = [O.solve_full_diagonalization(f, [2, 2, 2], [64, 64, 64], [1.0] * 3, 0.0) for f in fs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    bufs = []
+    for f in fs:
+        b = torch.zeros(tuple(spec.extents()[:-1]) + (plan.pitch,), dtype=torch.float64, device="cuda")
+        b[..., :f.shape[-1]] = torch.from_numpy(f)
+        bufs.append(b)
+    torch.cuda.synchronize()
+    for i, b in enumerate(bufs):
+        plan.solve_device(b.data_ptr(), plan.pitch, streams[i % 2].cuda_stream)
+    torch.cuda.synchronize()
+    for b, f, w in zip(bufs, fs, wants):
+        assert rel_l2(b[..., :f.shape[-1]].cpu().numpy(), w) <= TOL
