@@ -609,30 +609,64 @@ def table(n: int, K: int) -> Table:
 # ----------------------------------------------------------------------------
 
 
+# Short transforms are the O(K^2) sums themselves; from FAST_K on they go
+# through scipy.fft's r2r transforms, whose unnormalised type-I/II/III
+# definitions are FFTW's (the functions the reference binds, trig.cpp:43-48),
+# rescaled exactly as Plan::execute does (trig.cpp:71-92).  Both forms are
+# checked against each other and against the reference's trig KATs in
+# tests/test_oracle.py; the fast form makes 1e9-unknown full-size checks
+# feasible (C5 n=1, which the reference itself cannot run in 2-D/3-D).
+FAST_K = 48
+
+
+def _sfft():
+    try:
+        import scipy.fft as sf
+        return sf
+    except Exception:  # scipy absent: the direct sums only
+        return None
+
+
 def _sin_matrix(K):
     j = np.arange(1, K)
     return np.sin(np.pi * np.outer(j, j) / K)
 
 
-def dst1(x: np.ndarray) -> np.ndarray:
-    """X_k = sum_{j=1}^{K-1} x_j sin(pi j k / K) over the last axis (trig.hpp:4)."""
+def dst1(x: np.ndarray, direct: bool = False) -> np.ndarray:
+    """X_k = sum_{j=1}^{K-1} x_j sin(pi j k / K) over the last axis (trig.hpp:4).
+    FFTW RODFT00 output times 1/2 (trig.cpp:76-78)."""
     K = x.shape[-1] + 1
     if K == 1:
         return x.copy()
+    sf = _sfft()
+    if sf is not None and not direct and K >= FAST_K:
+        return 0.5 * sf.dst(x, type=1, axis=-1, workers=-1)
     return x @ _sin_matrix(K).T
 
 
-def dst3_synthesis(b: np.ndarray) -> np.ndarray:
-    """w_j = sum_{k=1}^{K} b_k sin(pi k (j-1/2)/K) (trig.hpp:5)."""
+def dst3_synthesis(b: np.ndarray, direct: bool = False) -> np.ndarray:
+    """w_j = sum_{k=1}^{K} b_k sin(pi k (j-1/2)/K) (trig.hpp:5).
+    FFTW RODFT01 of the input halved except the last (trig.cpp:83-91)."""
     K = b.shape[-1]
+    sf = _sfft()
+    if sf is not None and not direct and K >= FAST_K:
+        h = 0.5 * b
+        h[..., -1] = b[..., -1]
+        return sf.dst(h, type=3, axis=-1, workers=-1)
     j = np.arange(1, K + 1)
     k = np.arange(1, K + 1)
     return b @ np.sin(np.pi * np.outer(k, j - 0.5) / K)
 
 
-def dct3_synthesis(a: np.ndarray) -> np.ndarray:
-    """w_j = sum_{k=0}^{K-1} a_k cos(pi k (j-1/2)/K) (trig.hpp:6)."""
+def dct3_synthesis(a: np.ndarray, direct: bool = False) -> np.ndarray:
+    """w_j = sum_{k=0}^{K-1} a_k cos(pi k (j-1/2)/K) (trig.hpp:6).
+    FFTW REDFT01 of the input halved except the first (trig.cpp:83-91)."""
     K = a.shape[-1]
+    sf = _sfft()
+    if sf is not None and not direct and K >= FAST_K:
+        h = 0.5 * a
+        h[..., 0] = a[..., 0]
+        return sf.dct(h, type=3, axis=-1, workers=-1)
     j = np.arange(1, K + 1)
     k = np.arange(0, K)
     return a @ np.cos(np.pi * np.outer(k, j - 0.5) / K)

@@ -262,3 +262,51 @@ def test_reference_trig_invocation_counter():
             before = reflib.lib().sfemref_trig_invocations()
             reflib.lines(op, n, K, x)
             assert reflib.lib().sfemref_trig_invocations() - before == n
+
+
+@pytest.mark.parametrize("K", [48, 64, 100, 114, 256, 1024])
+def test_oracle_fast_trig_forms_match_direct_sums_and_reference(K):
+    # the scipy r2r forms (K >= FAST_K) against the O(K^2) sums and against the
+    # reference's own trig module (oracle/_ref: trig.cpp through the FFTW shim)
+    rng = np.random.default_rng(K)
+    x, b, a = rng.standard_normal(K - 1), rng.standard_normal(K), rng.standard_normal(K)
+    tol = 1e-13 * K
+    assert np.max(np.abs(O.dst1(x) - O.dst1(x, direct=True))) <= tol
+    assert np.max(np.abs(O.dst3_synthesis(b) - O.dst3_synthesis(b, direct=True))) <= tol
+    assert np.max(np.abs(O.dct3_synthesis(a) - O.dct3_synthesis(a, direct=True))) <= tol
+    if reflib.available():
+        assert np.max(np.abs(O.dst1(x) - reflib.trig(0, x))) <= 1e-13 * K
+        assert np.max(np.abs(O.dst3_synthesis(b) - reflib.trig(1, b))) <= 1e-13 * K
+        assert np.max(np.abs(O.dct3_synthesis(a) - reflib.trig(2, a))) <= 1e-13 * K
+
+
+@pytest.mark.skipif(not reflib.available(), reason="oracle/_ref not built")
+def test_oracle_fast_path_solves_match_reference():
+    # 3-D solves whose transforms take the fast forms, against the reference
+    for n, K in ((2, 64), (3, 48)):
+        ext = [n * K - 1] * 3
+        f = np.random.default_rng(n).uniform(-1, 1, ext)
+        u = O.solve_full_diagonalization(f, [n] * 3, [K] * 3, [1.0] * 3, 0.5)
+        want, _ = reflib.solve(f, [n] * 3, [K] * 3, [1.0] * 3, 0.5)
+        assert rel_l2(u, want) <= 1e-12
+
+
+def test_reference_cannot_solve_order1_beyond_1d():
+    # documents why C5 n = 1 is checked against the restatement: the
+    # reference's forward_axis computes rows = lines / row_len with row_len = 0
+    # for the zero-extent interior classes of an n = 1 axis (poisson.cpp:294-296),
+    # a SIGFPE.  Run in a child process so the crash cannot take pytest down.
+    import subprocess
+    import sys
+    if not reflib.available():
+        pytest.skip("oracle/_ref not built")
+    code = ("import numpy as np; from oracle import reflib; "
+            "reflib.solve(np.ones((7, 7)), [1, 1], [8, 8], [1.0, 1.0], 0.5)")
+    import os
+    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       capture_output=True)
+    assert r.returncode != 0
+    # the restatement handles it (and matches the 1-D reference, which does run)
+    f = np.random.default_rng(1).uniform(-1, 1, 7)
+    want, _ = reflib.solve(f, [1], [8], [1.0], 0.5)
+    assert rel_l2(O.solve_full_diagonalization(f, [1], [8], [1.0], 0.5), want) <= 1e-13
