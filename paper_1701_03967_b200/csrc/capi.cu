@@ -396,6 +396,21 @@ Step rows_step(const View& v, int mode) {
   return s;
 }
 
+// Row sweeps with per-row bulk copies: the fused forward + divide + inverse
+// runs the warp-local-job kernel (sweep_rows.cu) unless SFEM_ROWS_V1=1 selects
+// the block-synchronous one (sweep_fast.cu sweep_bulk_rows, kept for A/B).
+bool rows_v1() {
+  const char* e = std::getenv("SFEM_ROWS_V1");
+  return e && e[0] == '1';
+}
+
+cudaError_t launch_rows(const DevTable& dt, double* data, const RowSegs& rs, long long nrows, int mode,
+                        const SymbolInfo& sym, cudaStream_t stream) {
+  if (mode == kForwardDivideInverse && !rows_v1() && has_rows_fused(dt.n, dt.K))
+    return launch_sweep_rows_fused(dt, data, rs, nrows, sym, stream);
+  return launch_sweep_bulk_rows(dt, data, rs, nrows, mode, kWeighted, sym, stream);
+}
+
 // Launch a list of steps on `data` (in place).
 void launch_steps(std::vector<Step>& steps, double* user, sfem_ctx ctx, cudaStream_t stream,
                   std::vector<cudaEvent_t>* kev, double* scratch = nullptr) {
@@ -424,7 +439,7 @@ void launch_steps(std::vector<Step>& steps, double* user, sfem_ctx ctx, cudaStre
       rs.len[0] = static_cast<int>((dt.L + 1) & ~1);
       rs.off[0] = 0;
       rs.stride[0] = s.ls.os1;
-      ck(launch_sweep_bulk_rows(dt, data, rs, s.ls.nlines, s.mode, kWeighted, s.sym, stream), "bulk rows sweep launch");
+      ck(launch_rows(dt, data, rs, s.ls.nlines, s.mode, s.sym, stream), "bulk rows sweep launch");
     } else if (s.use_fast && has_fast_sweep(dt.n, dt.K, s.mode, s.ls.contiguous)) {
       ck(launch_sweep_fast(dt, s.ls, s.mode, kWeighted, sym, stream), "fast sweep launch");
     } else if (s.use_fast && has_mid_sweep(dt.n, dt.K)) {
@@ -1794,7 +1809,7 @@ int sfem_cuda_dist_phase(sfem_dist d, int phase, double* x, double* y, double* b
       case SFEM_DIST_AXIS0:
         if (d->fused_y) {
           const Step& st = d->phaseB[0];
-          ck(launch_sweep_bulk_rows(st.table->dev, buf, d->ysegs, lyR, kForwardDivideInverse, kWeighted, st.sym, s),
+          ck(launch_rows(st.table->dev, buf, d->ysegs, lyR, kForwardDivideInverse, st.sym, s),
              "axis0 (exchange buffer)");
         } else {
           launch_steps(d->phaseB, y, d->ctx, s, nullptr);

@@ -144,6 +144,11 @@ cudaError_t launch_peer_barrier(const PeerFlags& fl, int nranks, int rank, unsig
 cudaError_t launch_sweep_bulk_rows(const DevTable& t, double* data, const RowSegs& segs, long long nrows, int mode,
                                    int analysis, const SymbolInfo& sym, cudaStream_t stream);
 enum AnalysisKind { kWeighted = 0, kDirect = 1 };
+// Fused last-axis sweep (forward + divide + inverse) with warp-local FFT jobs
+// (sweep_rows.cu); same row segments as launch_sweep_bulk_rows.
+bool has_rows_fused(int n, int K);
+cudaError_t launch_sweep_rows_fused(const DevTable& t, double* data, const RowSegs& segs, long long nrows,
+                                    const SymbolInfo& sym, cudaStream_t stream);
 
 // Shared-memory bytes needed for a tile of B lines of table t (FFT work
 // buffers excluded when they live in global scratch).

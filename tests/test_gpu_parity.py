@@ -457,3 +457,24 @@ def test_plan_on_two_streams_is_ordered(sfem):
     torch.cuda.synchronize()
     for b, f, w in zip(bufs, fs, wants):
         assert rel_l2(b[..., :f.shape[-1]].cpu().numpy(), w) <= TOL
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 8, 9])
+def test_rows_fused_kernel_matches_block_sync_kernel(sfem, n, monkeypatch):
+    # the warp-local fused last-axis kernel (sweep_rows.cu) against the
+    # block-synchronous one (SFEM_ROWS_V1=1, sweep_fast.cu): same arithmetic
+    # in the same order, so bitwise equal; 3-D blocked schedule and 2-D rows,
+    # partial last tiles
+    for orders, elements in (([n, n, n], [64, 64, 64]) if n <= 4 else ([2, 3, n], [64, 5, 64]),
+                             ([3, n], [7, 64])):
+        N = len(orders)
+        spec = sfem.ProblemSpec(N, [1.0] * N, elements, orders, 0.3)
+        f = np.random.default_rng(n).uniform(-1, 1, spec.extents())
+        u_new, _ = sfem.solve_dof(spec, f)
+        monkeypatch.setenv("SFEM_ROWS_V1", "1")
+        u_old, _ = sfem.solve_dof(spec, f)
+        monkeypatch.delenv("SFEM_ROWS_V1")
+        assert np.array_equal(u_new, u_old), (orders, elements, float(np.max(np.abs(u_new - u_old))))
+        if np.prod(spec.extents()) < 3e6:
+            want = O.solve_full_diagonalization(f, orders, elements, [1.0] * N, 0.3)
+            assert rel_l2(u_new, want) <= TOL
