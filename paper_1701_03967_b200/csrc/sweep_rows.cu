@@ -43,8 +43,16 @@ namespace rows {
 using namespace reg;
 
 constexpr int N = 64, R = 8, G = 8, B = 8;
-constexpr int XJOB = 130;  // doubles per job slot: 65 complex (exchange) = 2 S rows of 65
+// Job slot: 68 complex.  The exchange X[q][c] (8 x 8 complex) is stored at
+// q*8 + (c ^ q), and consecutive jobs start 4 bank quads apart (68 = 4 mod 8):
+// the eight lanes of a 128-bit access phase (two jobs x four taus) then hit
+// eight distinct quads in both the pass-1 stores and the pass-2 loads.  The
+// job's two S rows (65 doubles each) start at +0 or +4 doubles (bit 1 of the
+// job index), so the 16 lanes of a 64-bit phase (four jobs x four taus) hit 16
+// distinct bank pairs in the S-row accesses.
+constexpr int XJOB = 136;  // doubles per job slot
 constexpr int SR = 65;     // doubles per S row (index k = 1..63 used)
+__host__ __device__ constexpr int sbase(int j) { return j * XJOB + 4 * ((j >> 1) & 1); }
 
 template <int V, int A>
 constexpr int round_up(int v = V) {
@@ -59,7 +67,7 @@ struct Cfg {
   static constexpr int NJOB = NPAIR + NNOD + NMID;
   static constexpr int PAIR_WARPS = NPAIR / 8;
   static constexpr int FFT_WARPS = (NJOB + 7) / 8;
-  static constexpr int ITEMS = (N - 1) * 2;  // mix items (k, 4-line group)
+  static constexpr int ITEMS = N * 2;  // mix item slots (k = 1..64, 4-line group); k = 64 is idle
   static constexpr int THREADS = (32 * FFT_WARPS > round_up<ITEMS + B, 32>()) ? 32 * FFT_WARPS
                                                                             : round_up<ITEMS + B, 32>();
   static constexpr int P = (L + 1) & ~1;                   // doubles per row copy (16-byte multiple)
@@ -144,10 +152,10 @@ __device__ __forceinline__ int pair_job(int i, int b) {
 template <int NN>
 __device__ __forceinline__ int srow(int s, int b) {
   using C = Cfg<NN>;
-  if (s == 0) return (C::NPAIR + b) * XJOB;  // nodal job (which = b >> 2, line pair b & 3)
-  if (C::MODD && s == 1 + C::HALF) return (C::NPAIR + C::NNOD + (b & 3)) * XJOB + (b >> 2) * SR;
-  if (s <= C::HALF) return pair_job<NN>(s - 1, b) * XJOB;
-  return pair_job<NN>(s - 1 - C::NE, b) * XJOB + SR;
+  if (s == 0) return sbase(C::NPAIR + b);  // nodal job (which = b >> 2, line pair b & 3)
+  if (C::MODD && s == 1 + C::HALF) return sbase(C::NPAIR + C::NNOD + (b & 3)) + (b >> 2) * SR;
+  if (s <= C::HALF) return sbase(pair_job<NN>(s - 1, b));
+  return sbase(pair_job<NN>(s - 1 - C::NE, b)) + SR;
 }
 
 // Partner value of output class member (h, P): pairing (q, R-q) with tau = 0
@@ -317,7 +325,7 @@ __device__ __forceinline__ void forward_job(const Job& jb, const double* T, doub
       const int c = h == 0 ? jb.c1 : jb.c2;
       Dft<R>::run(v[h]);
 #pragma unroll
-      for (int q = 0; q < R; ++q) Xj[q * G + c] = q == 0 ? v[h][q] : c_mul(v[h][q], tw[(c * q) % N]);
+      for (int q = 0; q < R; ++q) Xj[q * G + (c ^ q)] = q == 0 ? v[h][q] : c_mul(v[h][q], tw[(c * q) % N]);
     }
   }
   __syncwarp();
@@ -325,8 +333,8 @@ __device__ __forceinline__ void forward_job(const Job& jb, const double* T, doub
   if (jb.kind < 3) {
 #pragma unroll
     for (int c = 0; c < G; ++c) {
-      w1[c] = Xj[jb.q1 * G + c];
-      w2[c] = Xj[jb.q2 * G + c];
+      w1[c] = Xj[jb.q1 * G + (c ^ jb.q1)];
+      w2[c] = Xj[jb.q2 * G + (c ^ jb.q2)];
     }
   }
   __syncwarp();  // the warp's slots are read: S rows overwrite them
@@ -334,8 +342,8 @@ __device__ __forceinline__ void forward_job(const Job& jb, const double* T, doub
   Dft<G>::run(w1);
   Dft<G>::run(w2);
   if (jb.kind != 1) {
-    double* sA = X + jb.j * XJOB + SR;  // pair: H_k row (odd part); middle: line b + 4's row
-    double* sB = X + jb.j * XJOB;       // pair: G_{N-k} row (even part); middle: line b's row
+    double* sA = X + sbase(jb.j) + SR;  // pair: H_k row (odd part); middle: line b + 4's row
+    double* sB = X + sbase(jb.j);       // pair: G_{N-k} row (even part); middle: line b's row
     if (jb.kind == 2) {
       double* t_ = sA;
       sA = sB;
@@ -414,8 +422,8 @@ __device__ __forceinline__ void inverse_job(const Job& jb, double* T, double* X,
   } else if (jb.kind == 0 || jb.kind == 2) {
     // real part: DCT-III of a (pair: odd part of line b; middle: reversed even
     // slot of line b); imaginary part: DCT-III of b~ (reversed even slot)
-    const double* A = X + jb.j * XJOB + (jb.kind == 0 ? SR : 0);
-    const double* Bs = X + jb.j * XJOB + (jb.kind == 0 ? 0 : SR);
+    const double* A = X + sbase(jb.j) + (jb.kind == 0 ? SR : 0);
+    const double* Bs = X + sbase(jb.j) + (jb.kind == 0 ? 0 : SR);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = h == 0 ? jb.c1 : jb.c2;
@@ -450,7 +458,7 @@ __device__ __forceinline__ void inverse_job(const Job& jb, double* T, double* X,
       const int c = h == 0 ? jb.c1 : jb.c2;
       Dft<R>::run(v[h]);
 #pragma unroll
-      for (int q = 0; q < R; ++q) Xj[q * G + c] = q == 0 ? v[h][q] : c_mul(v[h][q], tw[(c * q) % N]);
+      for (int q = 0; q < R; ++q) Xj[q * G + (c ^ q)] = q == 0 ? v[h][q] : c_mul(v[h][q], tw[(c * q) % N]);
     }
   }
   __syncwarp();
@@ -458,8 +466,8 @@ __device__ __forceinline__ void inverse_job(const Job& jb, double* T, double* X,
   if (jb.kind < 3) {
 #pragma unroll
     for (int c = 0; c < G; ++c) {
-      w[0][c] = Xj[jb.q1 * G + c];
-      w[1][c] = Xj[jb.q2 * G + c];
+      w[0][c] = Xj[jb.q1 * G + (c ^ jb.q1)];
+      w[1][c] = Xj[jb.q2 * G + (c ^ jb.q2)];
     }
   }
   __syncthreads();  // (B4) every slot is read: the output tile overwrites them
@@ -543,8 +551,8 @@ template <int NN>
 __host__ __device__ constexpr int srow_c(int s, int b) {
   // constexpr twin of srow (same placement)
   using C = Cfg<NN>;
-  if (s == 0) return (C::NPAIR + b) * XJOB;
-  if (C::MODD && s == 1 + C::HALF) return (C::NPAIR + C::NNOD + (b & 3)) * XJOB + (b >> 2) * SR;
+  if (s == 0) return sbase(C::NPAIR + b);
+  if (C::MODD && s == 1 + C::HALF) return sbase(C::NPAIR + C::NNOD + (b & 3)) + (b >> 2) * SR;
   const bool odd = s > C::HALF + C::MODD;
   const int i = odd ? s - 1 - C::NE : s - 1;
   int j = 0;
@@ -554,7 +562,7 @@ __host__ __device__ constexpr int srow_c(int s, int b) {
   } else {
     j = i * B + b;
   }
-  return j * XJOB + (odd ? SR : 0);
+  return sbase(j) + (odd ? SR : 0);
 }
 
 template <int NN>
@@ -563,7 +571,9 @@ __device__ __forceinline__ void mix_item(int item, double* X, const double* __re
                                          const double* base, double f_last) {
   using C = Cfg<NN>;
   constexpr int M = C::M;
-  const int k = 1 + (item >> 1), g = item & 1;
+  // lanes 0-15 / 16-31 of a warp: the same 16 frequencies, line groups 0 / 1
+  // (one matrix load serves both halves; a 64-bit phase sees 16 distinct k)
+  const int k = 1 + (item & 15) + 16 * (item >> 5), g = (item >> 4) & 1;
   // S entry (s, line 4g + bb) of this k: one base pointer per slot class
   // (the line-group step is the same for all slots of a class), the rest
   // compile-time offsets
@@ -729,8 +739,9 @@ __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB)
   forward_job<NN>(jb, T, T, C0, tw, mkh, om);  // contains B1
   __syncthreads();                              // (B2) S rows and centre partials complete
 #ifndef SFEM_ROWS_DIAG_NOMIX
-  if (tid < C::ITEMS)
-    mix_item<NN>(tid, T, t.mixT_i, t.eig, t.nsq, base, sym.f_last);
+  if (tid < C::ITEMS) {
+    if ((tid & 15) + 16 * (tid >> 5) < N - 1) mix_item<NN>(tid, T, t.mixT_i, t.eig, t.nsq, base, sym.f_last);
+  }
 #else
   if (false) {
   }

@@ -20,10 +20,12 @@ def run(orders, reps=10):
     gen = torch.Generator(device="cuda")
     gen.manual_seed(0)
     base = torch.rand(rows, plan.pitch, dtype=torch.float64, device="cuda", generator=gen)
+    base[:, ext[-1]:] = 0
     out = {}
     for v1 in ("0", "1"):
         os.environ["SFEM_ROWS_V1"] = v1
         buf = base.clone()
+        torch.cuda.synchronize()  # the plan runs on its context stream
         plan.solve_device(buf.data_ptr())
         torch.cuda.synchronize()
         sol = buf.clone()
@@ -36,5 +38,15 @@ def run(orders, reps=10):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "once":  # one solve per kernel (for ncu)
+        spec = sfem.ProblemSpec(3, [1.0] * 3, [64] * 3, [9, 9, 9], 0.0)
+        plan = sfem.Plan(spec)
+        buf = torch.zeros(plan.unknowns // plan.extents[-1], plan.pitch, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        for v1 in ("0", "1"):
+            os.environ["SFEM_ROWS_V1"] = v1
+            plan.solve_device(buf.data_ptr())
+            torch.cuda.synchronize()
+        sys.exit(0)
     for o in ([9, 9, 9], [5, 5, 5], [2, 2, 2], [4, 4, 4], [7, 7, 7]):
         run(o)
