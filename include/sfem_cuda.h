@@ -103,6 +103,25 @@ enum { SFEM_OP_DECOMPOSE_WEIGHTED = 0, SFEM_OP_DECOMPOSE = 1, SFEM_OP_SYNTHESIZE
 enum { SFEM_OP_APPLY_MASS = 3, SFEM_OP_APPLY_STIFFNESS = 4 };
 int sfem_cuda_lines_device(sfem_table table, int op, long long count, const double* d_in,
                            long long in_pitch, double* d_out, long long out_pitch, void* stream);
+/* The same three transforms on lines with an element stride: position t of
+ * line b at d_in[t*pos_stride + b*line_stride] (and the same offsets in
+ * d_out; in place when d_in == d_out).  pos_stride = count, line_stride = 1 is
+ * the slot-major tile of the reference's batched kernels ("the value at
+ * position j of line b sits at [j*count + b]", eigenbasis.hpp:66-69) in the
+ * dof / coefficient layout; pos_stride = 1 is sfem_cuda_lines_device. */
+int sfem_cuda_lines_strided_device(sfem_table table, int op, long long count, const double* d_in, double* d_out,
+                                   long long pos_stride, long long line_stride, void* stream);
+/* lines::decompose_weighted_block / synthesize_block (eigenbasis.hpp:70-73,
+ * eigenbasis.cpp:248-444) with the reference's own arguments: slot-major
+ * class tiles, nodal (K+1) x count (boundary slots included; ignored by the
+ * analyses, written as 0 by the synthesis), interior K*(n-1) x count
+ * element-major (NULL for n = 1), coeffs (n*K-1) x count frequency-major,
+ * all addressed [j*count + b].  SFEM_OP_DECOMPOSE_WEIGHTED / _DECOMPOSE read
+ * the class tiles and write coeffs; SFEM_OP_SYNTHESIZE reads coeffs and
+ * writes the class tiles.  Any count >= 1 (the reference uses <= 32,
+ * poisson.cpp:231). */
+int sfem_cuda_lines_block_device(sfem_table table, int op, long long count, double* d_nodal, double* d_interior,
+                                 double* d_coeffs, void* stream);
 /* Same on host buffers (dense, pitch = L); host<->device copies included. */
 int sfem_cuda_lines_host(sfem_table table, int op, long long count, const double* h_in, double* h_out);
 /* materialize_eigenvector (spectral.hpp:330, spectral.cpp:238-265): the grid

@@ -91,6 +91,9 @@ _SIGS = [
      [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp, _dp, _dp]),
     ("sfem_cuda_lines_device", ctypes.c_int,
      [_vp, ctypes.c_int, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp, ctypes.c_longlong, _vp]),
+    ("sfem_cuda_lines_strided_device", ctypes.c_int,
+     [_vp, ctypes.c_int, ctypes.c_longlong, _vp, _vp, ctypes.c_longlong, ctypes.c_longlong, _vp]),
+    ("sfem_cuda_lines_block_device", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_longlong, _vp, _vp, _vp, _vp]),
     ("sfem_cuda_lines_host", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_longlong, _dp, _dp]),
     ("sfem_cuda_table_eigenvector", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _dp]),
     ("sfem_cuda_plan_create", ctypes.c_int,
@@ -362,6 +365,62 @@ def lines_device(table: SpectralTable, op: int, count: int, d_in: int, in_pitch:
     """Batched line transform on device pointers (sfem_cuda_lines_device)."""
     _check(lib.sfem_cuda_lines_device(table.handle, op, count, ctypes.c_void_p(d_in), in_pitch,
                                       ctypes.c_void_p(d_out), out_pitch, ctypes.c_void_p(stream or 0)))
+
+
+def lines_strided_device(table: SpectralTable, op: int, count: int, d_in: int, d_out: int, pos_stride: int,
+                         line_stride: int, stream: Optional[int] = None) -> None:
+    """Line transforms with an element stride (sfem_cuda_lines_strided_device);
+    pos_stride = count, line_stride = 1 is the reference's slot-major tile."""
+    _check(lib.sfem_cuda_lines_strided_device(table.handle, op, count, ctypes.c_void_p(d_in), ctypes.c_void_p(d_out),
+                                              pos_stride, line_stride, ctypes.c_void_p(stream or 0)))
+
+
+def lines_block_device(table: SpectralTable, op: int, count: int, d_nodal: int, d_interior: int, d_coeffs: int,
+                       stream: Optional[int] = None) -> None:
+    """lines::decompose_weighted_block / synthesize_block on device class tiles
+    (sfem_cuda_lines_block_device; eigenbasis.hpp:66-73)."""
+    _check(lib.sfem_cuda_lines_block_device(table.handle, op, count, ctypes.c_void_p(d_nodal),
+                                            ctypes.c_void_p(d_interior or 0), ctypes.c_void_p(d_coeffs),
+                                            ctypes.c_void_p(stream or 0)))
+
+
+def _block_tiles(table: SpectralTable, count: int):
+    n, K = table.order, table.elements
+    return (K + 1, count), (K * (n - 1), count), (n * K - 1, count)
+
+
+def decompose_weighted_block(table: SpectralTable, nodal: np.ndarray, interior: np.ndarray, count: int,
+                             op: int = DECOMPOSE_WEIGHTED) -> np.ndarray:
+    """lines::decompose_weighted_block (eigenbasis.cpp:248-331) on host tiles:
+    nodal (K+1, count), interior (K*(n-1), count) slot-major -> coeffs
+    (n*K-1, count).  op = DECOMPOSE gives the F_n analysis on the same tiles."""
+    import torch
+    sn, si, sc = _block_tiles(table, count)
+    nodal, interior = _f64(nodal).reshape(sn), _f64(interior).reshape(si)
+    with torch.cuda.device(table.ctx.device):
+        dn = torch.from_numpy(nodal).cuda()
+        di = torch.from_numpy(interior).cuda()
+        dc = torch.empty(sc, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        lines_block_device(table, op, count, dn.data_ptr(), di.data_ptr() if di.numel() else 0, dc.data_ptr())
+        torch.cuda.synchronize()
+        return dc.cpu().numpy()
+
+
+def synthesize_block(table: SpectralTable, coeffs: np.ndarray, count: int):
+    """lines::synthesize_block (eigenbasis.cpp:333-444): coeffs (n*K-1, count)
+    -> (nodal (K+1, count) with zero boundary slots, interior (K*(n-1), count))."""
+    import torch
+    sn, si, sc = _block_tiles(table, count)
+    coeffs = _f64(coeffs).reshape(sc)
+    with torch.cuda.device(table.ctx.device):
+        dc = torch.from_numpy(coeffs).cuda()
+        dn = torch.full(sn, float("nan"), dtype=torch.float64, device="cuda")
+        di = torch.empty(si, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        lines_block_device(table, SYNTHESIZE, count, dn.data_ptr(), di.data_ptr() if di.numel() else 0, dc.data_ptr())
+        torch.cuda.synchronize()
+        return dn.cpu().numpy(), di.cpu().numpy()
 
 
 def synthesize(coeffs: CoefficientArray1D, table: SpectralTable) -> GridFunction1D:

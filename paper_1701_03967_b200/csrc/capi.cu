@@ -1295,6 +1295,30 @@ int sfem_cuda_table_export(sfem_table t, double* values, double* norm_sq, double
   });
 }
 
+namespace {
+// One line transform (op = SFEM_OP_DECOMPOSE_WEIGHTED / DECOMPOSE / SYNTHESIZE)
+// over a LineSet with the fastest kernel compiled for the table.
+void launch_lines(sfem_table t, const LineSet& ls, int op, cudaStream_t s) {
+  const int mode = op == SFEM_OP_SYNTHESIZE ? kInverse : kForward;
+  const int analysis = op == SFEM_OP_DECOMPOSE ? kDirect : kWeighted;
+  const long long count = ls.nlines;
+  if (fast_enabled() && has_fast_sweep(t->dev.n, t->dev.K, mode, ls.contiguous)) {
+    ck(launch_sweep_fast(t->dev, ls, mode, analysis, nullptr, s), "lines launch (fast)");
+  } else if (fast_enabled() && has_mid_sweep(t->dev.n, t->dev.K)) {
+    const size_t wd = mid_work_doubles(t->dev.n, t->dev.K, count);
+    double* gw = wd ? scratch_for(t->ctx, wd, s) : nullptr;
+    ck(launch_sweep_mid(t->dev, ls, mode, analysis, nullptr, s, gw), "lines launch (mid)");
+    if (gw) scratch_done(t->ctx, s);
+  } else {
+    bool gwork = false;
+    const int B = choose_tile(t->dev, count, &gwork);
+    double* gw = gwork ? scratch_for(t->ctx, sweep_work_doubles(t->dev, B) * ((count + B - 1) / B), s) : nullptr;
+    ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s, gw), "lines launch");
+    if (gw) scratch_done(t->ctx, s);
+  }
+}
+}  // namespace
+
 int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* d_in, long long in_pitch,
                            double* d_out, long long out_pitch, void* stream) {
   return guarded([&] {
@@ -1347,21 +1371,86 @@ int sfem_cuda_lines_device(sfem_table t, int op, long long count, const double* 
     ls.os2 = 0;
     ls.ps = 1;
     ls.contiguous = 1;
-    const int mode = op == SFEM_OP_SYNTHESIZE ? kInverse : kForward;
-    const int analysis = op == SFEM_OP_DECOMPOSE ? kDirect : kWeighted;
-    if (fast_enabled() && has_fast_sweep(t->dev.n, t->dev.K, mode, 1)) {
-      ck(launch_sweep_fast(t->dev, ls, mode, analysis, nullptr, s), "lines launch (fast)");
-    } else if (fast_enabled() && has_mid_sweep(t->dev.n, t->dev.K)) {
-      const size_t wd = mid_work_doubles(t->dev.n, t->dev.K, count);
-      double* gw = wd ? scratch_for(t->ctx, wd, s) : nullptr;
-      ck(launch_sweep_mid(t->dev, ls, mode, analysis, nullptr, s, gw), "lines launch (mid)");
-      if (gw) scratch_done(t->ctx, s);
+    launch_lines(t, ls, op, s);
+  });
+}
+
+int sfem_cuda_lines_strided_device(sfem_table t, int op, long long count, const double* d_in, double* d_out,
+                                   long long pos_stride, long long line_stride, void* stream) {
+  return guarded([&] {
+    require(t != nullptr, "lines: null table");
+    require(op >= SFEM_OP_DECOMPOSE_WEIGHTED && op <= SFEM_OP_SYNTHESIZE, "lines_strided: unknown op");
+    require(count >= 0, "lines: negative count");
+    require(d_in && d_out, "lines_strided: null buffer");
+    require(pos_stride >= 1 && line_stride >= 1, "lines_strided: strides must be positive");
+    const long long L = t->dev.L;
+    // the (position, line) index map must be one-to-one
+    require((pos_stride >= count * line_stride) || (line_stride >= L * pos_stride),
+            "lines_strided: lines overlap (need pos_stride >= count*line_stride or line_stride >= L*pos_stride)");
+    if (count == 0) return;
+    if (pos_stride == 1) {  // rows: the line-major entry
+      if (sfem_cuda_lines_device(t, op, count, d_in, line_stride, d_out, line_stride, stream) != 0)
+        throw std::runtime_error(g_err);
+      return;
+    }
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->ctx->stream;
+    ck(cudaSetDevice(t->ctx->device), "cudaSetDevice");
+    LineSet ls{};
+    ls.src = d_in;
+    ls.dst = d_out;
+    ls.nlines = count;
+    ls.ninner = count;
+    ls.n1 = 1;
+    ls.is = line_stride;
+    ls.os1 = 0;
+    ls.os2 = 0;
+    ls.ps = pos_stride;
+    ls.contiguous = 0;
+    launch_lines(t, ls, op, s);
+  });
+}
+
+int sfem_cuda_lines_block_device(sfem_table t, int op, long long count, double* d_nodal, double* d_interior,
+                                 double* d_coeffs, void* stream) {
+  return guarded([&] {
+    require(t != nullptr, "lines: null table");
+    require(op >= SFEM_OP_DECOMPOSE_WEIGHTED && op <= SFEM_OP_SYNTHESIZE, "lines_block: unknown op");
+    require(count >= 0, "lines: negative count");
+    const int n = t->dev.n, K = t->dev.K;
+    require(d_nodal && d_coeffs && (d_interior || n == 1), "lines_block: null tile");
+    if (count == 0) return;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->ctx->stream;
+    ck(cudaSetDevice(t->ctx->device), "cudaSetDevice");
+    const long long L = t->dev.L;
+    LineSet ls{};
+    ls.nlines = count;
+    ls.ninner = count;
+    ls.n1 = 1;
+    ls.is = 1;
+    ls.os1 = 0;
+    ls.os2 = 0;
+    ls.ps = count;
+    ls.contiguous = 0;
+    if (op != SFEM_OP_SYNTHESIZE) {
+      // class tiles -> dof tile (in the coefficient tile's storage: same shape), transformed in place
+      ck(launch_class_tiles(n, K, count, d_nodal, d_interior, d_coeffs, true, s), "lines_block: gather");
+      ls.src = d_coeffs;
+      ls.dst = d_coeffs;
+      launch_lines(t, ls, op, s);
     } else {
-      bool gwork = false;
-      const int B = choose_tile(t->dev, count, &gwork);
-      double* gw = gwork ? scratch_for(t->ctx, sweep_work_doubles(t->dev, B) * ((count + B - 1) / B), s) : nullptr;
-      ck(launch_sweep(t->dev, ls, mode, analysis, nullptr, B, s, gw), "lines launch");
-      if (gw) scratch_done(t->ctx, s);
+      // coefficients stay untouched: the sweep writes a temporary dof tile
+      double* tmp = nullptr;
+      ck(cudaMallocAsync(&tmp, static_cast<size_t>(L) * count * sizeof(double), s), "lines_block: cudaMallocAsync");
+      ls.src = d_coeffs;
+      ls.dst = tmp;
+      try {
+        launch_lines(t, ls, op, s);
+        ck(launch_class_tiles(n, K, count, d_nodal, d_interior, tmp, false, s), "lines_block: scatter");
+      } catch (...) {
+        cudaFreeAsync(tmp, s);
+        throw;
+      }
+      ck(cudaFreeAsync(tmp, s), "lines_block: cudaFreeAsync");
     }
   });
 }

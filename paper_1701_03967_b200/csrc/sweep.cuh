@@ -170,6 +170,11 @@ size_t mid_work_doubles(int n, int K, long long nlines);
 cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& lines, int mode, int analysis,
                              const SymbolInfo* sym, cudaStream_t stream, double* gwork = nullptr);
 
+// Slot-major class tiles (nodal (K+1) x count, interior K*(n-1) x count,
+// [j*count + b]) <-> the slot-major dof tile (n*K-1) x count (lines_block.cu).
+cudaError_t launch_class_tiles(int n, int K, long long count, double* nodal, double* interior, double* dof,
+                               bool to_dof, cudaStream_t stream);
+
 // Launch one sweep over `lines` with tiles of B lines.
 cudaError_t launch_sweep(const DevTable& t, const LineSet& lines, int mode, int analysis,
                          const SymbolInfo* sym, int B, cudaStream_t stream, double* gwork = nullptr);

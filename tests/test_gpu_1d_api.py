@@ -84,3 +84,80 @@ def test_weighted_analysis_of_mass_times_eigenvector_is_indicator(sfem, n, K):
             want = np.zeros_like(c)
             want[sfem.CoefficientArray1D.zeros(n, K).index(k, l)] = 1.0
             assert np.max(np.abs(c - want)) <= 1e-11
+
+
+# ---- slot-major batched line API (lines::*_block, eigenbasis.hpp:66-73) ----
+
+def _class_tiles(x, n, K):
+    """dof-layout lines (count, nK-1) -> slot-major (nodal (K+1, count), interior (K(n-1), count))."""
+    count, m = x.shape[0], n - 1
+    nodal = np.zeros((K + 1, count))
+    inter = np.zeros((K * m, count))
+    for t in range(n * K - 1):
+        e, c = divmod(t, n)
+        if c == m:
+            nodal[e + 1] = x[:, t]
+        else:
+            inter[e * m + c] = x[:, t]
+    return nodal, inter
+
+
+@needs_ref
+@pytest.mark.parametrize("n,K,count", [(1, 8, 5), (2, 64, 32), (3, 7, 1), (9, 64, 32), (4, 256, 19), (5, 12, 32),
+                                        (9, 114, 7), (2, 512, 40)])
+def test_block_api_matches_reference_block_kernels(sfem, n, K, count):
+    # the reference's own batched kernels on the same slot-major tiles
+    # (decompose_weighted_block / synthesize_block, eigenbasis.cpp:248-444)
+    t = sfem.SpectralTable(n, K)
+    rng = np.random.default_rng(n * 1000 + K + count)
+    x = rng.uniform(-1, 1, (count, n * K - 1))
+    nodal, inter = _class_tiles(x, n, K)
+    nodal[0] = rng.uniform(-1, 1, count)   # boundary slots are ignored by the analyses
+    nodal[K] = rng.uniform(-1, 1, count)
+    got = sfem.decompose_weighted_block(t, nodal, inter, count)
+    want = reflib.lines("decompose_weighted_block", n, K, x).T
+    assert got.shape == (n * K - 1, count)
+    assert np.linalg.norm(got - want) <= 1e-11 * np.linalg.norm(want)
+    # F_n on the same tiles (the reference has the per-line form only)
+    got_d = sfem.decompose_weighted_block(t, nodal, inter, count, op=sfem.DECOMPOSE)
+    want_d = reflib.lines("decompose", n, K, x).T
+    assert np.linalg.norm(got_d - want_d) <= 1e-11 * np.linalg.norm(want_d)
+    # synthesis back into class tiles: boundary slots written as zero
+    c = rng.uniform(-1, 1, (count, n * K - 1))
+    gn, gi = sfem.synthesize_block(t, c.T.copy(), count)
+    wn, wi = _class_tiles(reflib.lines("synthesize_block", n, K, c), n, K)
+    assert np.all(gn[0] == 0.0) and np.all(gn[K] == 0.0)
+    assert np.linalg.norm(gn - wn) <= 1e-11 * np.linalg.norm(wn)
+    if n > 1:
+        assert np.linalg.norm(gi - wi) <= 1e-11 * np.linalg.norm(wi)
+
+
+@pytest.mark.parametrize("n,K,count", [(9, 64, 32), (4, 256, 8), (3, 10, 5)])
+def test_strided_lines_match_line_major(sfem, n, K, count):
+    # the slot-major dof tile [t*count + b] and a general (pos, line) stride
+    # pair give the line-major results (bitwise for the same kernel family is
+    # not required: different tile shapes; 1e-13 relative)
+    import torch
+    t = sfem.SpectralTable(n, K)
+    L = n * K - 1
+    x = np.random.default_rng(L + count).uniform(-1, 1, (count, L))
+    for op in (sfem.DECOMPOSE_WEIGHTED, sfem.DECOMPOSE, sfem.SYNTHESIZE):
+        want = sfem.lines(t, op, x)
+        d = torch.from_numpy(x.T.copy()).cuda()          # (L, count): pos_stride = count
+        torch.cuda.synchronize()
+        sfem.lines_strided_device(t, op, count, d.data_ptr(), d.data_ptr(), count, 1)
+        torch.cuda.synchronize()
+        got = d.cpu().numpy().T
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want), op
+        # out of place, padded strides: position stride count + 3, line stride 1
+        src = torch.zeros((L, count + 3), dtype=torch.float64, device="cuda")
+        src[:, :count] = torch.from_numpy(x.T.copy())
+        dst = torch.full((L, count + 3), 7.0, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        sfem.lines_strided_device(t, op, count, src.data_ptr(), dst.data_ptr(), count + 3, 1)
+        torch.cuda.synchronize()
+        out = dst.cpu().numpy()
+        assert np.linalg.norm(out[:, :count].T - want) <= 1e-13 * np.linalg.norm(want), op
+        assert np.all(out[:, count:] == 7.0)
+    with pytest.raises(sfem.Error):
+        sfem.lines_strided_device(t, 0, count, d.data_ptr(), d.data_ptr(), count - 1 if count > 1 else 0, 1)
