@@ -255,6 +255,35 @@ int sfem_cuda_dist_destroy(sfem_dist dist);
 int sfem_cuda_dist_shape(sfem_dist dist, long long* info, long long* send_counts, long long* recv_counts);
 int sfem_cuda_dist_phase(sfem_dist dist, int phase, double* d_x, double* d_y, double* d_buf, void* stream);
 
+/* ---- The same slab solve with the library owning the exchange (NCCL) ----
+ * A C or C++ host needs no collective of its own: the plan creates an NCCL
+ * communicator from a unique id (made on one rank by sfem_cuda_nccl_unique_id
+ * and handed to the others by whatever the host uses: MPI, a socket, a file),
+ * allocates the exchange buffers and the y-slab, and one call runs the whole
+ * solve on this rank's x-slab d_x ([lx][L1]..[L_{N-1}], last axis padded to
+ * xpitch; in place).  Both all-to-all exchanges are grouped ncclSend/ncclRecv
+ * on a second stream, split into `chunks` pieces (0 = default 4; fewer if the
+ * in-place axis-0 sweep would need more than 32 row segments) so that chunk c
+ * travels over NVLink while chunk c+1 is swept: exchange 1 behind the forward
+ * sweeps of x-row chunks, exchange 2 behind the fused axis-0 sweeps of y-row
+ * chunks.  libnccl.so.2 is opened at run time (dlopen), not linked.
+ * Replaces run_full_diagonalization (poisson.cpp:637-669), sharded. */
+#define SFEM_NCCL_UNIQUE_ID_BYTES 128
+int sfem_cuda_nccl_unique_id(void* id /* SFEM_NCCL_UNIQUE_ID_BYTES */);
+int sfem_cuda_dist_comm_init(sfem_dist dist, const void* id, int chunks);
+int sfem_cuda_dist_solve(sfem_dist dist, double* d_x, void* stream);
+/* After a solve: phase_ms[6] = {forward local + pack, exchange 1 left exposed,
+ * axis 0, exchange 2 left exposed, unpack + inverse local, whole solve} from
+ * CUDA events (synchronises on the last one) and the bytes this rank sent to
+ * other ranks per solve.  Either pointer may be NULL. */
+int sfem_cuda_dist_solve_stats(sfem_dist dist, double* phase_ms, long long* bytes_sent);
+/* Chunk schedule and buffers without a communicator, and all `n` ranks of a
+ * solve run in one process on one device with the messages moved by device
+ * copies (the single-GPU check of the chunked schedule: same phases, chunks and
+ * message lists as sfem_cuda_dist_solve). */
+int sfem_cuda_dist_setup(sfem_dist dist, int chunks);
+int sfem_cuda_dist_solve_group(sfem_dist* dists, int n, double* const* d_xs, void* stream);
+
 /* ---- Multi-GPU with the exchanges fused into the sweeps over NVLink ----
  * 3-D problems whose axes 0 and 1 have K = 64 tables (config 4), 1..8 ranks,
  * one process per GPU.  No NCCL on the data path: the axis-1 forward sweep

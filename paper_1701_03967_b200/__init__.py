@@ -130,6 +130,12 @@ _SIGS = [
     ("sfem_cuda_dist_destroy", ctypes.c_int, [_vp]),
     ("sfem_cuda_dist_shape", ctypes.c_int, [_vp, _llp, _llp, _llp]),
     ("sfem_cuda_dist_phase", ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    ("sfem_cuda_nccl_unique_id", ctypes.c_int, [_vp]),
+    ("sfem_cuda_dist_comm_init", ctypes.c_int, [_vp, _vp, ctypes.c_int]),
+    ("sfem_cuda_dist_solve", ctypes.c_int, [_vp, _vp, _vp]),
+    ("sfem_cuda_dist_solve_stats", ctypes.c_int, [_vp, _dp, _llp]),
+    ("sfem_cuda_dist_setup", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("sfem_cuda_dist_solve_group", ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, ctypes.POINTER(_vp), _vp]),
 ]
 HEADER_SYMBOLS = [s[0] for s in _SIGS]
 for _name, _res, _args in _SIGS:

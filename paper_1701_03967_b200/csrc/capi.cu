@@ -14,6 +14,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and prototypes only: the library is dlopen-ed (libnccl.so.2), never linked
 
 #include <algorithm>
 #include <chrono>
@@ -940,6 +942,20 @@ struct sfem_dist_s {
   View xv, yv;
   std::vector<Step> phaseA, phaseB, phaseC;
   SlabView sv{};
+  // ---- library-owned solve (sfem_cuda_dist_solve): buffers, chunk schedule, communicator ----
+  int C = 0;                                  // chunks per exchange (0 = not set up)
+  std::vector<std::vector<long long>> xc0, xw;  // [rank][chunk]: chunk rows of that rank's x-slab (even starts)
+  std::vector<std::vector<long long>> yc0, yw;  // [rank][chunk]: chunk rows of that rank's y range
+  std::vector<std::vector<Step>> stepsA;      // forward local, per x-chunk
+  std::vector<SlabView> svc;                  // slab transposes, per x-chunk
+  std::vector<std::vector<Step>> stepsB;      // axis 0, per y-chunk (y-slab path)
+  std::vector<RowSegs> segsB;                 // axis 0 in place on the exchange buffer, per y-chunk (K = 64 path)
+  double *bufA = nullptr, *bufB = nullptr, *ybuf = nullptr;
+  ncclComm_t comm = nullptr;
+  cudaStream_t cs = nullptr;                  // exchange stream
+  std::vector<cudaEvent_t> ev;                // 2C + 2 events
+  double phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long bytes_sent = 0;                   // per solve, to other ranks (NVLink)
 };
 
 namespace {
@@ -1835,10 +1851,15 @@ int sfem_cuda_dist_create(sfem_ctx ctx, int dim, const int* orders, const int* e
   });
 }
 
+namespace {
+void dist_teardown(sfem_dist_s* d);
+}
+
 int sfem_cuda_dist_destroy(sfem_dist d) {
   return guarded([&] {
     if (!d) return;
     cudaSetDevice(d->ctx->device);
+    dist_teardown(d);
     for (auto& t : d->owned)
       if (t->dbuf) cudaFree(t->dbuf);
     delete d;
@@ -1926,6 +1947,442 @@ int sfem_cuda_dist_phase(sfem_dist d, int phase, double* x, double* y, double* b
   });
 }
 
+
+// ---------------------------------------------------------------------------
+// Library-owned distributed solve: NCCL communicator, buffers and the chunked
+// exchange schedule behind one call (sfem_cuda_dist_solve).
+//
+// Both exchanges are split into C chunks so that NVLink traffic overlaps the
+// sweeps that produce it:
+//   exchange 1: the x-slab is cut into C row chunks (even starts).  Chunk c is
+//     swept forward (rows + strided axes 1..N-2), transposed into its part of
+//     buffer A ([Q][wp_c] at A + Q*xc0_c, destination-major blocks) and handed
+//     to the exchange stream, which sends it while chunk c+1 is swept.  The
+//     receiver stores the block of (source s, chunk c) at
+//     B + lyR*(x0_s + xc0_{s,c}): the y-slab row q is then the concatenation
+//     of one segment per (source, chunk), which is what the axis-0 sweep reads
+//     (RowSegs, K = 64 tables) or UNPACK1 copies into the y-slab.
+//   exchange 2: the rank's y range is cut into C chunks; after the fused
+//     axis-0 sweep of chunk c, its rows of every (destination, x-chunk) block
+//     go back while chunk c+1 is swept.  They land in A where PACK1 read them.
+// Messages between a pair of ranks are issued in the same order on both sides
+// (x-chunk ascending), inside one ncclGroup per chunk.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclGetVersion) GetVersion = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // a process that already loaded NCCL (torch) keeps its copy: same soname
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (a.h) break;
+    }
+    if (!a.h) return a;
+    auto sym = [&](const char* n) { return dlsym(a.h, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.GetVersion = reinterpret_cast<decltype(a.GetVersion)>(sym("ncclGetVersion"));
+    return a;
+  }();
+  require(api.h && api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+              api.GroupEnd,
+          "NCCL: libnccl.so.2 could not be loaded (it is opened at run time; put it on the library path)");
+  return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    const char* msg = nccl().GetErrorString ? nccl().GetErrorString(r) : "error";
+    fail(std::string("NCCL: ") + what + ": " + msg);
+  }
+}
+
+long long even_up(long long v) { return v + (v & 1); }
+
+// One message of an exchange chunk: `count` doubles at `off` of the local
+// send (or receive) buffer, to (from) rank `peer`.
+struct Msg {
+  int peer;
+  long long off, count;
+};
+
+// Exchange 1, x-chunk c: what rank r sends / receives.
+void msgs1(const sfem_dist_s* d, int r, int c, std::vector<Msg>& sends, std::vector<Msg>& recvs) {
+  const long long Q = d->ext[1] * d->R;
+  sends.clear();
+  recvs.clear();
+  const long long w = d->xw[r][c], wp = even_up(w);
+  for (int p = 0; p < d->nranks; ++p) {
+    if (w > 0 && d->ly[p] > 0)
+      sends.push_back({p, Q * d->xc0[r][c] + d->y0[p] * d->R * wp, d->ly[p] * d->R * wp});
+    const long long ws = d->xw[p][c];
+    if (ws > 0 && d->ly[r] > 0)
+      recvs.push_back({p, d->ly[r] * d->R * (d->x0[p] + d->xc0[p][c]), d->ly[r] * d->R * even_up(ws)});
+  }
+}
+
+// Exchange 2, y-chunk c of the sender: rank r's sends (from B, as the y-side
+// rank) and receives (into A, as the x-side rank), x-chunk ascending per peer.
+void msgs2(const sfem_dist_s* d, int r, int c, std::vector<Msg>& sends, std::vector<Msg>& recvs) {
+  const long long Q = d->ext[1] * d->R;
+  sends.clear();
+  recvs.clear();
+  const long long lyR = d->ly[r] * d->R;
+  for (int p = 0; p < d->nranks; ++p)
+    for (int cx = 0; cx < d->C; ++cx) {
+      const long long wpp = even_up(d->xw[p][cx]);
+      if (d->xw[p][cx] > 0 && d->yw[r][c] > 0)
+        sends.push_back({p, lyR * (d->x0[p] + d->xc0[p][cx]) + d->yc0[r][c] * d->R * wpp, d->yw[r][c] * d->R * wpp});
+      const long long wpr = even_up(d->xw[r][cx]);
+      if (d->xw[r][cx] > 0 && d->yw[p][c] > 0)
+        recvs.push_back({p, Q * d->xc0[r][cx] + (d->y0[p] + d->yc0[p][c]) * d->R * wpr, d->yw[p][c] * d->R * wpr});
+    }
+}
+
+long long dist_buf_elems(const sfem_dist_s* d) {
+  long long sx = 0, rx = 0;
+  const int r = d->rank;
+  for (int p = 0; p < d->nranks; ++p) {
+    sx += d->lxp[r] * d->ly[p] * d->R;
+    rx += d->lxp[p] * d->ly[r] * d->R;
+  }
+  return std::max<long long>(std::max(sx, rx), 2);
+}
+
+// Chunk schedule and plan-owned buffers (idempotent for the same C).
+void dist_setup(sfem_dist_s* d, int chunks) {
+  require(chunks >= 1 && chunks <= 16, "dist: chunks must be in 1..16");
+  if (d->C == chunks) return;
+  require(d->C == 0, "dist: the chunk count of a set-up plan cannot change");
+  ck(cudaSetDevice(d->ctx->device), "cudaSetDevice");
+  const int P = d->nranks, r = d->rank, dim = d->dim;
+  int C = chunks;
+  if (d->fused_y) {
+    int nonempty = 0;
+    for (int p = 0; p < P; ++p) nonempty += d->lx[p] > 0;
+    while (C > 1 && nonempty * C > kMaxSeg) --C;
+  }
+  d->xc0.assign(P, {});
+  d->xw.assign(P, {});
+  d->yc0.assign(P, {});
+  d->yw.assign(P, {});
+  for (int p = 0; p < P; ++p) {
+    d->xw[p] = balanced_even(d->lx[p], C, d->xc0[p]);
+    d->yw[p] = balanced(d->ly[p], C, d->yc0[p]);
+  }
+  d->C = C;
+  const std::vector<long long> st = d->xv.strides();
+  d->stepsA.assign(C, {});
+  d->svc.assign(C, SlabView{});
+  for (int c = 0; c < C; ++c) {
+    View v = d->xv;
+    v.ext[0] = d->xw[r][c];
+    if (v.ext[0] > 0) {
+      d->stepsA[c].push_back(rows_step(v, kForward));
+      for (int a = dim - 2; a >= 1; --a) d->stepsA[c].push_back(strided_step(v, a, kForward));
+    }
+    SlabView sv = d->sv;
+    sv.lx = d->xw[r][c];
+    sv.bpitch = even_up(sv.lx);
+    d->svc[c] = sv;
+  }
+  d->stepsB.assign(C, {});
+  d->segsB.assign(C, RowSegs{});
+  const long long lyR = d->ly[r] * d->R;
+  for (int c = 0; c < C; ++c) {
+    if (d->yw[r][c] == 0) continue;
+    if (d->fused_y) {
+      RowSegs& rs = d->segsB[c];
+      rs.n = 0;
+      for (int p = 0; p < P; ++p)
+        for (int cx = 0; cx < C; ++cx) {
+          if (d->xw[p][cx] == 0) continue;
+          const long long wp = even_up(d->xw[p][cx]);
+          rs.pos0[rs.n] = static_cast<int>(d->x0[p] + d->xc0[p][cx]);
+          rs.len[rs.n] = static_cast<int>(wp);
+          rs.off[rs.n] = lyR * (d->x0[p] + d->xc0[p][cx]) + d->yc0[r][c] * d->R * wp;
+          rs.stride[rs.n] = wp;
+          ++rs.n;
+        }
+    }
+    View v = d->yv;
+    v.ext[0] = d->yw[r][c];
+    v.eig_off[0] = d->y0[r] + d->yc0[r][c];
+    d->stepsB[c].push_back(rows_step(v, kForwardDivideInverse));
+  }
+  const size_t nb = static_cast<size_t>(dist_buf_elems(d)) * sizeof(double);
+  ck(cudaMalloc(&d->bufA, nb), "dist: cudaMalloc (exchange buffer A)");
+  ck(cudaMalloc(&d->bufB, nb), "dist: cudaMalloc (exchange buffer B)");
+  ck(cudaMemset(d->bufA, 0, nb), "dist: memset");
+  ck(cudaMemset(d->bufB, 0, nb), "dist: memset");
+  if (!d->fused_y && lyR > 0) {
+    const size_t ny = static_cast<size_t>(lyR) * d->ypitch * sizeof(double);
+    ck(cudaMalloc(&d->ybuf, ny), "dist: cudaMalloc (y-slab)");
+    ck(cudaMemset(d->ybuf, 0, ny), "dist: memset");
+  }
+  ck(cudaStreamCreateWithFlags(&d->cs, cudaStreamNonBlocking), "dist: stream");
+  d->ev.resize(2 * C + 8);
+  for (auto& e : d->ev) ck(cudaEventCreate(&e), "dist: event");
+  (void)st;
+}
+
+void dist_teardown(sfem_dist_s* d) {
+  if (d->comm) {
+    nccl().CommDestroy(d->comm);
+    d->comm = nullptr;
+  }
+  for (auto& e : d->ev) cudaEventDestroy(e);
+  d->ev.clear();
+  if (d->cs) cudaStreamDestroy(d->cs);
+  d->cs = nullptr;
+  for (double** b : {&d->bufA, &d->bufB, &d->ybuf}) {
+    if (*b) cudaFree(*b);
+    *b = nullptr;
+  }
+}
+
+// The compute of one rank between the exchanges, chunk by chunk (stream s).
+void dist_forward_chunk(sfem_dist_s* d, double* x, int c, cudaStream_t s) {
+  const int r = d->rank;
+  if (d->xw[r][c] == 0) return;
+  const long long st0 = d->xv.strides()[0];
+  const long long Q = d->ext[1] * d->R;
+  double* xc = x + d->xc0[r][c] * st0;
+  launch_steps(d->stepsA[c], xc, d->ctx, s, nullptr);
+  ck(launch_slab_transpose(d->svc[c], xc, d->bufA + Q * d->xc0[r][c], true, s), "slab transpose");
+}
+
+void dist_unpack1(sfem_dist_s* d, cudaStream_t s) {
+  if (d->fused_y) return;
+  const int r = d->rank;
+  const long long lyR = d->ly[r] * d->R;
+  if (lyR == 0) return;
+  for (int p = 0; p < d->nranks; ++p)
+    for (int cx = 0; cx < d->C; ++cx) {
+      const long long w = d->xw[p][cx];
+      if (w == 0) continue;
+      const long long pos = d->x0[p] + d->xc0[p][cx];
+      ck(cudaMemcpy2DAsync(d->ybuf + pos, d->ypitch * sizeof(double), d->bufB + lyR * pos,
+                           even_up(w) * sizeof(double), w * sizeof(double), lyR, cudaMemcpyDeviceToDevice, s),
+         "unpack1");
+    }
+}
+
+void dist_axis0_chunk(sfem_dist_s* d, int c, cudaStream_t s) {
+  const int r = d->rank;
+  const long long nq = d->yw[r][c] * d->R;
+  if (nq == 0) return;
+  if (d->fused_y) {
+    const Step& st = d->stepsB[c][0];
+    ck(launch_rows(st.table->dev, d->bufB, d->segsB[c], nq, kForwardDivideInverse, st.sym, s),
+       "axis0 (exchange buffer)");
+    return;
+  }
+  const long long lyR = d->ly[r] * d->R;
+  const long long q0 = d->yc0[r][c] * d->R;
+  launch_steps(d->stepsB[c], d->ybuf + q0 * d->ypitch, d->ctx, s, nullptr);
+  for (int p = 0; p < d->nranks; ++p)  // PACK2 of the chunk's rows
+    for (int cx = 0; cx < d->C; ++cx) {
+      const long long w = d->xw[p][cx];
+      if (w == 0) continue;
+      const long long pos = d->x0[p] + d->xc0[p][cx], wp = even_up(w);
+      ck(cudaMemcpy2DAsync(d->bufB + lyR * pos + q0 * wp, wp * sizeof(double), d->ybuf + q0 * d->ypitch + pos,
+                           d->ypitch * sizeof(double), w * sizeof(double), nq, cudaMemcpyDeviceToDevice, s),
+         "pack2");
+    }
+}
+
+void dist_inverse(sfem_dist_s* d, double* x, cudaStream_t s) {
+  const int r = d->rank;
+  const long long st0 = d->xv.strides()[0];
+  const long long Q = d->ext[1] * d->R;
+  for (int c = 0; c < d->C; ++c) {
+    if (d->xw[r][c] == 0) continue;
+    ck(launch_slab_transpose(d->svc[c], x + d->xc0[r][c] * st0, d->bufA + Q * d->xc0[r][c], false, s),
+       "slab transpose");
+  }
+  launch_steps(d->phaseC, x, d->ctx, s, nullptr);
+}
+
+void nccl_exchange(sfem_dist_s* d, const std::vector<Msg>& sends, const double* sbuf, const std::vector<Msg>& recvs,
+                   double* rbuf) {
+  NcclApi& n = nccl();
+  nck(n.GroupStart(), "ncclGroupStart");
+  for (const Msg& m : sends)
+    nck(n.Send(sbuf + m.off, static_cast<size_t>(m.count), ncclDouble, m.peer, d->comm, d->cs), "ncclSend");
+  for (const Msg& m : recvs)
+    nck(n.Recv(rbuf + m.off, static_cast<size_t>(m.count), ncclDouble, m.peer, d->comm, d->cs), "ncclRecv");
+  nck(n.GroupEnd(), "ncclGroupEnd");
+}
+
+}  // namespace
+
+int sfem_cuda_nccl_unique_id(void* id) {
+  return guarded([&] {
+    require(id != nullptr, "nccl_unique_id: null argument");
+    static_assert(sizeof(ncclUniqueId) == SFEM_NCCL_UNIQUE_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId u;
+    nck(nccl().GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof u);
+  });
+}
+
+int sfem_cuda_dist_setup(sfem_dist d, int chunks) {
+  return guarded([&] {
+    require(d != nullptr, "dist_setup: null plan");
+    dist_setup(d, chunks > 0 ? chunks : 4);
+  });
+}
+
+int sfem_cuda_dist_comm_init(sfem_dist d, const void* id, int chunks) {
+  return guarded([&] {
+    require(d && id, "dist_comm_init: null argument");
+    require(d->comm == nullptr, "dist_comm_init: the plan already has a communicator");
+    dist_setup(d, chunks > 0 ? chunks : (d->C > 0 ? d->C : 4));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    nck(nccl().CommInitRank(&d->comm, d->nranks, u, d->rank), "ncclCommInitRank");
+  });
+}
+
+int sfem_cuda_dist_solve(sfem_dist d, double* d_x, void* stream) {
+  return guarded([&] {
+    require(d && d->comm, "dist_solve: no communicator (call sfem_cuda_dist_comm_init first)");
+    require(d_x != nullptr || d->lx[d->rank] == 0, "dist_solve: null x-slab");
+    ck(cudaSetDevice(d->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    const int C = d->C, r = d->rank;
+    std::vector<Msg> sends, recvs;
+    cudaEvent_t* ev = d->ev.data();
+    cudaEvent_t *t0 = ev + 2 * C, *t1 = t0 + 1, *t2 = t0 + 2, *t3 = t0 + 3, *t4 = t0 + 4, *t5 = t0 + 5;
+    long long sent = 0;
+    ck(cudaEventRecord(*t0, s), "event");
+    ck(cudaStreamWaitEvent(d->cs, *t0, 0), "wait");  // the exchange stream starts behind earlier work on s
+    for (int c = 0; c < C; ++c) {
+      dist_forward_chunk(d, d_x, c, s);
+      ck(cudaEventRecord(ev[c], s), "event");
+      ck(cudaStreamWaitEvent(d->cs, ev[c], 0), "wait");
+      msgs1(d, r, c, sends, recvs);
+      for (const Msg& m : sends) sent += m.peer != r ? m.count : 0;
+      nccl_exchange(d, sends, d->bufA, recvs, d->bufB);
+    }
+    ck(cudaEventRecord(*t1, s), "event");  // forward compute done
+    ck(cudaEventRecord(*t2, d->cs), "event");
+    ck(cudaStreamWaitEvent(s, *t2, 0), "wait");  // exchange 1 complete
+    dist_unpack1(d, s);
+    for (int c = 0; c < C; ++c) {
+      dist_axis0_chunk(d, c, s);
+      ck(cudaEventRecord(ev[C + c], s), "event");
+      ck(cudaStreamWaitEvent(d->cs, ev[C + c], 0), "wait");
+      msgs2(d, r, c, sends, recvs);
+      for (const Msg& m : sends) sent += m.peer != r ? m.count : 0;
+      nccl_exchange(d, sends, d->bufB, recvs, d->bufA);
+    }
+    ck(cudaEventRecord(*t3, s), "event");  // axis-0 compute done
+    ck(cudaEventRecord(*t4, d->cs), "event");
+    ck(cudaStreamWaitEvent(s, *t4, 0), "wait");  // exchange 2 complete
+    dist_inverse(d, d_x, s);
+    ck(cudaEventRecord(*t5, s), "event");
+    d->bytes_sent = sent * static_cast<long long>(sizeof(double));
+  });
+}
+
+int sfem_cuda_dist_solve_stats(sfem_dist d, double* phase_ms, long long* bytes_sent) {
+  return guarded([&] {
+    require(d && d->C > 0 && d->ev.size() >= static_cast<size_t>(2 * d->C + 6), "dist_solve_stats: plan not set up");
+    ck(cudaSetDevice(d->ctx->device), "cudaSetDevice");
+    cudaEvent_t* t = d->ev.data() + 2 * d->C;
+    ck(cudaEventSynchronize(t[5]), "event sync");
+    auto ms = [&](int a, int b) {
+      float v = 0;
+      ck(cudaEventElapsedTime(&v, t[a], t[b]), "elapsed");
+      return static_cast<double>(v);
+    };
+    if (phase_ms) {
+      phase_ms[0] = ms(0, 1);  // forward local + pack (all chunks)
+      phase_ms[1] = ms(1, 2);  // exchange 1 not hidden behind the forward sweeps
+      phase_ms[2] = ms(2, 3);  // (unpack +) axis 0 (+ pack), all chunks
+      phase_ms[3] = ms(3, 4);  // exchange 2 not hidden behind the axis-0 sweeps
+      phase_ms[4] = ms(4, 5);  // unpack + inverse local
+      phase_ms[5] = ms(0, 5);  // whole solve
+    }
+    if (bytes_sent) *bytes_sent = d->bytes_sent;
+  });
+}
+
+// All ranks of a solve in one process on one device (the single-GPU check of
+// the chunk schedule): same phases, chunks and message lists as
+// sfem_cuda_dist_solve, the messages moved by device copies.  Messages of a
+// pair are matched in issue order, as NCCL matches them.
+int sfem_cuda_dist_solve_group(sfem_dist* ds, int n, double* const* d_xs, void* stream) {
+  return guarded([&] {
+    require(ds && d_xs && n >= 1, "dist_solve_group: null argument");
+    for (int r = 0; r < n; ++r) {
+      require(ds[r] && ds[r]->nranks == n && ds[r]->rank == r, "dist_solve_group: plans must be ranks 0..n-1 of n");
+      require(ds[r]->C > 0 && ds[r]->C == ds[0]->C, "dist_solve_group: set the plans up with one chunk count");
+      require(ds[r]->ctx->device == ds[0]->ctx->device, "dist_solve_group: one device");
+    }
+    ck(cudaSetDevice(ds[0]->ctx->device), "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ds[0]->ctx->stream;
+    const int C = ds[0]->C;
+    std::vector<std::vector<Msg>> sends(n), recvs(n);
+    auto exchange = [&](int step) {
+      for (int dst = 0; dst < n; ++dst)
+        for (int src = 0; src < n; ++src) {
+          std::vector<const Msg*> out, in;
+          for (const Msg& m : sends[src])
+            if (m.peer == dst) out.push_back(&m);
+          for (const Msg& m : recvs[dst])
+            if (m.peer == src) in.push_back(&m);
+          require(out.size() == in.size(), "dist_solve_group: send / receive lists disagree");
+          for (size_t i = 0; i < out.size(); ++i) {
+            require(out[i]->count == in[i]->count, "dist_solve_group: message sizes disagree");
+            const double* sb = step == 1 ? ds[src]->bufA : ds[src]->bufB;
+            double* rb = step == 1 ? ds[dst]->bufB : ds[dst]->bufA;
+            ck(cudaMemcpyAsync(rb + in[i]->off, sb + out[i]->off, out[i]->count * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s),
+               "dist_solve_group: copy");
+          }
+        }
+    };
+    for (int c = 0; c < C; ++c) {
+      for (int r = 0; r < n; ++r) {
+        dist_forward_chunk(ds[r], d_xs[r], c, s);
+        msgs1(ds[r], r, c, sends[r], recvs[r]);
+      }
+      exchange(1);
+    }
+    for (int r = 0; r < n; ++r) dist_unpack1(ds[r], s);
+    for (int c = 0; c < C; ++c) {
+      for (int r = 0; r < n; ++r) {
+        dist_axis0_chunk(ds[r], c, s);
+        msgs2(ds[r], r, c, sends[r], recvs[r]);
+      }
+      exchange(2);
+    }
+    for (int r = 0; r < n; ++r) dist_inverse(ds[r], d_xs[r], s);
+  });
+}
 
 int sfem_cuda_fem_load(sfem_plan p, int field, const double* params, int nparams, double* d_load, long long pitch,
                        void* stream) {

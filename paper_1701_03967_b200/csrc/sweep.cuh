@@ -101,7 +101,7 @@ bool has_tma_sweep(int n, int K);
 // is a plain dof tensor; the multi-GPU axis-0 sweep reads and writes the
 // source-major blocks of the exchange buffer directly.  In place.  `mode`:
 // kForward / kInverse / kForwardDivideInverse (sym used by the latter only).
-constexpr int kMaxSeg = 8;
+constexpr int kMaxSeg = 32;  // ranks x exchange chunks (multi-GPU axis-0 sweep)
 struct RowSegs {
   int n;
   int pos0[kMaxSeg], len[kMaxSeg];

@@ -114,6 +114,30 @@ class DistPlan:
     def phase(self, name: str, x: int, y: int, buf: int, stream: int = 0):
         _check(lib.sfem_cuda_dist_phase(self.handle, PHASES[name], _vp(x), _vp(y), _vp(buf), _vp(stream or None)))
 
+    # ---- library-owned exchange (NCCL inside the C-ABI, chunk-pipelined) ----
+    def setup(self, chunks: int = 0):
+        """Chunk schedule and plan-owned buffers without a communicator
+        (for solve_group)."""
+        _check(lib.sfem_cuda_dist_setup(self.handle, chunks))
+
+    def comm_init(self, unique_id: bytes, chunks: int = 0):
+        """Create the plan's NCCL communicator from a unique id made by
+        nccl_unique_id() on one rank (sfem_cuda_dist_comm_init)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), NCCL_UNIQUE_ID_BYTES)
+        _check(lib.sfem_cuda_dist_comm_init(self.handle, buf, chunks))
+
+    def solve(self, x_ptr: int, stream: int = 0):
+        """One whole distributed solve of this rank's x-slab, in place
+        (sfem_cuda_dist_solve: sweeps + grouped ncclSend/ncclRecv)."""
+        _check(lib.sfem_cuda_dist_solve(self.handle, _vp(x_ptr), _vp(stream or None)))
+
+    def stats(self):
+        """(phase_ms[6], bytes sent to other ranks) of the last solve."""
+        ms = (ctypes.c_double * 6)()
+        nb = ctypes.c_longlong()
+        _check(lib.sfem_cuda_dist_solve_stats(self.handle, ms, ctypes.byref(nb)))
+        return list(ms), nb.value
+
     def __del__(self):
         try:
             if self.handle:
@@ -121,6 +145,25 @@ class DistPlan:
                 self.handle = None
         except Exception:
             pass
+
+
+NCCL_UNIQUE_ID_BYTES = 128
+STAT_NAMES = ("forward_local+pack", "exchange1_exposed", "axis0", "exchange2_exposed", "unpack+inverse_local", "solve")
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    _check(lib.sfem_cuda_nccl_unique_id(buf))
+    return buf.raw
+
+
+def solve_group(plans: Sequence[DistPlan], x_ptrs, stream: int = 0):
+    """All ranks of a solve on one device, messages by device copies
+    (sfem_cuda_dist_solve_group; plans set up with one chunk count)."""
+    n = len(plans)
+    hs = (_vp * n)(*[p.handle for p in plans])
+    xs = (_vp * n)(*[_vp(int(x)) for x in x_ptrs])
+    _check(lib.sfem_cuda_dist_solve_group(hs, n, xs, _vp(stream or None)))
 
 
 def solve_ranks(plans: Sequence[DistPlan], xs, bufs_a, bufs_b, ys, exchange):

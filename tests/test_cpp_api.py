@@ -27,3 +27,27 @@ def test_cpp_mirror_parity(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+SRC2 = os.path.join(ROOT, "tests", "cpp", "test_dist_block.cpp")
+
+
+def build_c_abi_host(out):
+    subprocess.run(["g++", "-std=c++17", "-O2", SRC2, "-I", os.path.join(ROOT, "include"),
+                    "-I", "/usr/local/cuda/include", "-L", LIBDIR, "-lsfem_b200", "-L", "/usr/local/cuda/lib64",
+                    "-lcudart", f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", out], check=True)
+
+
+def test_c_abi_host_compiles_and_links(tmp_path):
+    build_c_abi_host(str(tmp_path / "test_dist_block"))
+
+
+@pytest.mark.gpu
+def test_c_abi_host_block_api_and_nccl_solve(tmp_path):
+    # a torch-free C++ host: slot-major block API + a 1-rank solve whose NCCL
+    # communicator and exchange live inside the C-ABI
+    exe = str(tmp_path / "test_dist_block")
+    build_c_abi_host(exe)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr

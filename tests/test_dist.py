@@ -298,3 +298,70 @@ def test_peer_bind_exchanges_handles_gloo(world):
             off = 0 if qq == r else 10 ** 6
             assert xs[qq] == off + base + 1 and ys[qq] == off + base + 2 and fs[qq] == off + base + 3
         assert len(opened) == 3 * (world - 1)
+
+
+# ---- library-owned exchange: chunked schedule (sfem_cuda_dist_solve*) ------
+
+def _group_solve(sfem, spec, P, chunks, f):
+    from paper_1701_03967_b200 import dist as D
+    plans = [D.DistPlan(spec, P, r) for r in range(P)]
+    xs = []
+    for p in plans:
+        p.setup(chunks)
+        x = torch.zeros(max(p.x_elems, 1), dtype=torch.float64, device="cuda")
+        D.scatter_x(p, x, f)
+        xs.append(x)
+    torch.cuda.synchronize()
+    D.solve_group(plans, [x.data_ptr() for x in xs])
+    torch.cuda.synchronize()
+    return np.concatenate([D.gather_x(p, x) for p, x in zip(plans, xs)], axis=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,chunks", [(1, 1), (1, 3), (2, 2), (3, 4), (5, 2), (8, 4), (8, 1)])
+@pytest.mark.parametrize("orders,elements,lengths,shift", [
+    ([2, 3, 2], [16, 9, 5], [1.0, 2.0, 1.0], 0.5),     # y-slab path (UNPACK1 / PACK2 per chunk)
+    ([3, 2, 4], [64, 7, 6], [1.0, 1.0, 2.0], 0.0),     # K = 64 on axis 0: axis 0 in place on the exchange buffer
+    ([9, 9], [64, 64], [1.0, 1.0], 1.0),               # 2-D, K = 64
+    ([4, 2], [32, 40], [1.0, 0.5], 0.25),              # 2-D, mid kernels
+])
+def test_chunked_group_solve_matches_single_gpu(sfem, P, chunks, orders, elements, lengths, shift):
+    spec = sfem.ProblemSpec(len(orders), lengths, elements, orders, shift)
+    f = np.random.default_rng(10 * P + chunks).uniform(-1, 1, spec.extents())
+    want, _ = sfem.solve_dof(spec, f)
+    got = _group_solve(sfem, spec, P, chunks, f)
+    assert rel_l2(got, want) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_chunked_group_solve_config4_p8(sfem):
+    spec = sfem.ProblemSpec(3, [1.0] * 3, [64] * 3, [9] * 3, 0.0)
+    f = np.random.default_rng(4).uniform(-1, 1, spec.extents())
+    want, _ = sfem.solve_dof(spec, f)
+    got = _group_solve(sfem, spec, 8, 4, f)
+    assert rel_l2(got, want) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("orders,elements,chunks", [([2, 3, 2], [16, 9, 5], 3), ([9, 9], [64, 64], 2)])
+def test_nccl_owned_solve_one_rank(sfem, orders, elements, chunks):
+    # the C-ABI's own communicator (ncclCommInitRank from a unique id) and
+    # grouped ncclSend / ncclRecv to self, on the exchange stream
+    from paper_1701_03967_b200 import dist as D
+    N = len(orders)
+    spec = sfem.ProblemSpec(N, [1.0] * N, elements, orders, 0.5)
+    f = np.random.default_rng(2).uniform(-1, 1, spec.extents())
+    want, _ = sfem.solve_dof(spec, f)
+    p = D.DistPlan(spec, 1, 0)
+    p.comm_init(D.nccl_unique_id(), chunks)
+    x = torch.zeros(p.x_elems, dtype=torch.float64, device="cuda")
+    D.scatter_x(p, x, f)
+    torch.cuda.synchronize()
+    for _ in range(2):  # buffers and events are reused
+        D.scatter_x(p, x, f)
+        torch.cuda.synchronize()
+        p.solve(x.data_ptr())
+        ms, sent = p.stats()
+        assert rel_l2(D.gather_x(p, x), want) <= 1e-13
+    assert sent == 0 and ms[5] > 0 and abs(sum(ms[:5]) - ms[5]) <= 0.05 * ms[5] + 0.05
