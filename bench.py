@@ -375,6 +375,26 @@ def run_peer(args, world, rank, local, dist):
     hbm_bytes = 16.0 * local_u * 5  # five sweeps, each reads and writes the rank's share once
     achieved = hbm_bytes / (ms_step * 1e-3) / 1e9
     nvl_bytes = 2 * 8.0 * local_u * (world - 1) / world
+    # per-rank phase times (one more solve, events between the phases) and the
+    # bytes this rank's two exchange sweeps store into other ranks' slabs
+    names = ("forward(rows + axis-1 sweep storing to peers)", "barrier1", "axis0(fused, storing back to peers)",
+             "barrier2", "inverse(axis 1 + rows)")
+    pev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    barrier(dist, world)
+    pev[0].record(ext)
+    for i, ph in enumerate((D.PEER_FORWARD, D.PEER_BARRIER, D.PEER_AXIS0, D.PEER_BARRIER, D.PEER_INVERSE)):
+        plan.phase(ph, ctx.stream)
+        pev[i + 1].record(ext)
+    torch.cuda.synchronize()
+    L0 = plan.extents[0]
+    mine = {"rank": rank, "unknowns": plan.lx * L1 * L2,
+            "nvlink_bytes_per_solve": 8 * L2 * (plan.lx * (L1 - plan.ly) + plan.ly * (L0 - plan.lx)),
+            "phase_ms": {nm: round(pev[i].elapsed_time(pev[i + 1]), 4) for i, nm in enumerate(names)}}
+    per_rank = [None] * world
+    if world > 1:
+        dist.all_gather_object(per_rank, mine)
+    else:
+        per_rank = [mine]
 
     h_in = torch.from_numpy(f_local).pin_memory()
     h_out = torch.empty_like(h_in).pin_memory()
@@ -403,6 +423,7 @@ def run_peer(args, world, rank, local, dist):
                          "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
                          "kernel": "whole per-rank solve (5 sweeps, 2 of them storing to peers)",
                          "nvlink_bytes_per_rank_per_solve": nvl_bytes},
+            "per_rank": per_rank,
             "cpu_baseline": None,
             "e2e": {"value": U / e2e_s, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * int(f_local.size) * world,
                     "d2h_bytes_per_step": 8 * int(f_local.size) * world, "ms_per_step": e2e_s * 1e3},
@@ -414,10 +435,13 @@ def run_peer(args, world, rank, local, dist):
 
 
 def run_distributed(args, world, rank, local, dist):
-    """N > 1: ONE global problem, slab-decomposed over the ranks (axis-0 slabs,
-    two NCCL all-to-all transposes per solve; paper_1701_03967_b200/dist.py).
-    Strong scaling: value = global unknowns / max-over-ranks time."""
-    import ctypes
+    """N > 1: ONE global problem, slab-decomposed over the ranks (axis-0 slabs).
+    The exchange lives inside the C-ABI (sfem_cuda_dist_solve): an NCCL
+    communicator created from a unique id that rank 0 makes and
+    torch.distributed only broadcasts, grouped ncclSend/ncclRecv on an exchange
+    stream, both all-to-alls split into chunks that travel while the next
+    chunk is swept.  Strong scaling: value = global unknowns / max-over-ranks
+    time.  Per-rank NVLink bytes and phase times are printed for every rank."""
     import torch
     import paper_1701_03967_b200 as sfem
     from paper_1701_03967_b200 import dist as D
@@ -426,15 +450,50 @@ def run_distributed(args, world, rank, local, dist):
     spec = sfem.ProblemSpec(len(orders), lengths, elements, orders, shift, coefficients=coeffs)
     ctx = sfem.Context(local)
     plan = D.DistPlan(spec, world, rank, ctx)
+    ids = [D.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(ids, src=0)
+    plan.comm_init(ids[0], args.dist_chunks)
     U = int(np.prod(plan.extents))
-    x, a, b, y = D.allocate(plan)
+    x = torch.zeros(max(plan.x_elems, 1), dtype=torch.float64, device=f"cuda:{local}")
+    inner = [int(v) for v in plan.extents[1:]]
     rows_local = plan.lx * int(np.prod(plan.extents[1:-1]))
     f_local = np.random.default_rng(1000 + rank).uniform(-1.0, 1.0, (rows_local, plan.extents[-1]))
-    x.view(-1, plan.xpitch)[:rows_local, :plan.extents[-1]].copy_(torch.from_numpy(f_local))
+    xview = x.view(-1, plan.xpitch)[:rows_local, :plan.extents[-1]]
+    xview.copy_(torch.from_numpy(f_local))
     ext = torch.cuda.ExternalStream(ctx.stream)
+    torch.cuda.synchronize()
 
     def solve():
-        D.solve_ranks([plan], [x], [a], [b], [y], D.torch_exchange)
+        plan.solve(x.data_ptr(), ctx.stream)
+
+    check = None
+    if not args.no_verify:
+        # rank 0's slab against a single-GPU solve of the same global load;
+        # every rank reaches the one all-reduce whatever happened locally
+        err = 0.0
+        try:
+            solve()
+            torch.cuda.synchronize()
+            mine = xview.cpu().numpy().reshape([plan.lx] + inner)
+            if rank == 0:
+                offs, lens = D.partition_even(plan.extents[0], world)
+                glob = np.concatenate([np.random.default_rng(1000 + r).uniform(
+                    -1.0, 1.0, (lens[r] * int(np.prod(plan.extents[1:-1])), plan.extents[-1]))
+                    for r in range(world)]).reshape(plan.extents)
+                want, _ = sfem.solve_dof(spec, glob, ctx=ctx)
+                want = want[offs[0]:offs[0] + lens[0]]
+                err = float(np.linalg.norm(mine - want) / np.linalg.norm(want))
+                del glob, want
+        except Exception as e:
+            print(f"[bench] rank {rank}: NCCL slab solve check failed locally: {e!r}", file=sys.stderr)
+            err = float("inf")
+        err = max_over_ranks(err, dist, world)
+        if not err <= 1e-11:
+            raise RuntimeError(f"NCCL slab solve differs from the single-GPU solve (rank-0 slab rel-L2 {err:.3e})")
+        check = f"rank-0 slab vs single-GPU solve of the same global load: rel-L2 {err:.2e}"
+        xview.copy_(torch.from_numpy(f_local))
+        torch.cuda.synchronize()
 
     for _ in range(args.warmup):
         solve()
@@ -445,6 +504,7 @@ def run_distributed(args, world, rank, local, dist):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         time.sleep(0.3)
+        barrier(dist, world)
         ev0.record(ext)
         for _ in range(args.steps):
             solve()
@@ -452,6 +512,14 @@ def run_distributed(args, world, rank, local, dist):
         torch.cuda.synchronize()
     barrier(dist, world)
     ms = max_over_ranks(ev0.elapsed_time(ev1), dist, world)
+    phase_ms, sent = plan.stats()  # of the last timed solve
+    mine = {"rank": rank, "nvlink_bytes_per_solve": sent, "unknowns": plan.lx * int(np.prod(plan.extents[1:])),
+            "phase_ms": dict(zip(D.STAT_NAMES, [round(v, 4) for v in phase_ms]))}
+    per_rank = [None] * world
+    if world > 1:
+        dist.all_gather_object(per_rank, mine)
+    else:
+        per_rank = [mine]
     value = U * args.steps / (ms * 1e-3)
     ms_step = ms / args.steps
     peaks, peak_kind = measured_peaks()
@@ -461,7 +529,6 @@ def run_distributed(args, world, rank, local, dist):
     sweep_bytes = 16.0 * local_u * (2 * len(orders) - 1)
     copy_bytes = 16.0 * local_u * (2 if plan.y_elems == 0 else 4)
     achieved = (sweep_bytes + copy_bytes) / (ms_step * 1e-3) / 1e9
-    a2a_bytes = 2 * 8.0 * sum(c for i, c in enumerate(plan.send_counts) if i != rank)
 
     # end to end: each rank moves its own slab host -> device -> host
     h_in = torch.from_numpy(f_local).pin_memory()
@@ -470,10 +537,10 @@ def run_distributed(args, world, rank, local, dist):
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         with torch.cuda.stream(ext):
-            x.view(-1, plan.xpitch)[:rows_local, :plan.extents[-1]].copy_(h_in, non_blocking=True)
+            xview.copy_(h_in, non_blocking=True)
         solve()
         with torch.cuda.stream(ext):
-            h_out.copy_(x.view(-1, plan.xpitch)[:rows_local, :plan.extents[-1]], non_blocking=True)
+            h_out.copy_(xview, non_blocking=True)
         torch.cuda.synchronize()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, dist, world)
     if rank == 0:
@@ -482,16 +549,21 @@ def run_distributed(args, world, rank, local, dist):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "unknowns": U, "extents": plan.extents,
-                       "parallelism": f"slab x{world} (axis-0 slabs, 2 NCCL all-to-all per solve)",
+                       "parallelism": f"slab x{world} (axis-0 slabs; 2 all-to-all exchanges per solve as grouped "
+                                      f"ncclSend/ncclRecv inside the C-ABI, {args.dist_chunks or 4} chunks "
+                                      "pipelined behind the sweeps)",
+                       "dist_check": check,
+                       "dist_error": getattr(args, "dist_error", None),
                        "l2_flush": "none needed: tensors > L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
                          "kernel": "whole per-rank solve (sweeps + transposes)",
-                         "nvlink_bytes_per_rank_per_solve": a2a_bytes},
+                         "nvlink_bytes_per_rank_per_solve": max(r["nvlink_bytes_per_solve"] for r in per_rank)},
+            "per_rank": per_rank,
             "cpu_baseline": None,
             "e2e": {"value": U / e2e_s, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * int(f_local.size) * world,
                     "d2h_bytes_per_step": 8 * int(f_local.size) * world, "ms_per_step": e2e_s * 1e3},
-            "gpu_launches": 7 * args.steps,
+            "gpu_launches": (2 * len(orders) + 1 + 2 * (args.dist_chunks or 4)) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -511,6 +583,8 @@ def main():
                     help="N > 1: skip the set-up check of the fused exchange against a single-GPU solve")
     ap.add_argument("--dist-mode", default="peer", choices=["peer", "nccl"],
                     help="N > 1: exchanges fused into the sweeps over NVLink peer memory, or NCCL all-to-all")
+    ap.add_argument("--dist-chunks", type=int, default=0,
+                    help="exchange chunks of the NCCL slab path (0 = the library default, 4)")
     ap.add_argument("--dist-single", action="store_true",
                     help="exercise the slab-decomposed path on one GPU (1-rank NCCL group)")
     args = ap.parse_args()

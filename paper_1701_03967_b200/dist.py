@@ -366,9 +366,12 @@ def ipc_open(handle: bytes) -> int:
     return out.value
 
 
-def peer_bind_distributed(plan: PeerPlan, dist_mod) -> None:
+def peer_bind_distributed(plan: PeerPlan, dist_mod, device_barrier: bool = True) -> None:
     """Exchange the ranks' buffer handles over torch.distributed and bind the
-    peers (one process per GPU, NVLink P2P)."""
+    peers (one process per GPU, NVLink P2P).  device_barrier=False binds no
+    flag words: the caller orders the phases from the host (stream
+    synchronise + a host barrier), as the two-processes-on-one-GPU test does,
+    where kernels of different processes must not wait on one another."""
     mine = [ipc_handle(plan.x_ptr), ipc_handle(plan.y_ptr), ipc_handle(plan.flags_ptr)]
     allh = [None] * plan.nranks
     dist_mod.all_gather_object(allh, mine)
@@ -380,7 +383,17 @@ def peer_bind_distributed(plan: PeerPlan, dist_mod) -> None:
         ptrs = [ipc_open(h) for h in hs]
         plan._opened += ptrs
         xs.append(ptrs[0]), ys.append(ptrs[1]), fs.append(ptrs[2])
-    plan.bind(xs, ys, fs)
+    plan.bind(xs, ys, fs if device_barrier else None)
+
+
+def peer_solve_host_ordered(plan: PeerPlan, dist_mod, stream: int = 0) -> None:
+    """One solve with the exchanges ordered from the host: every rank finishes
+    a phase (stream synchronise) and meets the others at a host barrier before
+    the next one starts.  No kernel waits for another process."""
+    for ph in (PEER_FORWARD, PEER_AXIS0, PEER_INVERSE):
+        plan.phase(ph, stream)
+        plan.barrier_timeout(stream)  # synchronises the stream
+        dist_mod.barrier()
 
 
 def peer_solve_loopback(plans: Sequence[PeerPlan], stream: int = 0) -> None:
