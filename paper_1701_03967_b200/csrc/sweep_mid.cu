@@ -2,6 +2,8 @@
 // the tuned shapes are instantiated here, the general shapes in
 // sweep_mid_k{16,...,2048}.cu (powers of two) and sweep_mid_k{24,...,1000}.cu
 // (3 * 2^j, 5 * 2^j, 2^i * 5^j), one translation unit per K, built in parallel.
+#include <cstdlib>
+
 #include "sweep_mid_impl.cuh"
 
 namespace sfem_b200 {
@@ -123,8 +125,22 @@ bool has_mid_sweep(int n, int K) {
          (n == 9 && K == 1024) || (n == 4 && K == 4096) || mid_auto(n, K);
 }
 
+// C2 (n = 4, K = 4096): one-line tiles with the packed middle / nodal job keep
+// the FFT work in shared memory (mid::Cfg::PK); SFEM_C2_GW=1 selects the older
+// kernel with the work in global scratch (kept for A/B).
+#ifndef SFEM_MID_C2_PK_TH
+#define SFEM_MID_C2_PK_TH 768
+#endif
+static bool c2_gw() {
+  static const bool v = [] {
+    const char* e = std::getenv("SFEM_C2_GW");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 size_t mid_work_doubles(int n, int K, long long nlines) {
-  if (n == 4 && K == 4096) {  // B = 1: jobs = 1 pair + 1 middle + 2 nodal
+  if (n == 4 && K == 4096 && c2_gw()) {  // B = 1: jobs = 1 pair + 1 middle + 2 nodal
     return static_cast<size_t>(nlines) * 2 * 2 * 4 * 4096;
   }
   return 0;
@@ -134,6 +150,7 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& ls, int mode, int
                              cudaStream_t stream, double* gwork) {
   if (ls.nlines <= 0) return cudaSuccess;
   if (t.n == 4 && t.K == 4096) {
+    if (!c2_gw()) return mid::launch<4, 4096, 1, SFEM_MID_C2_PK_TH>(t, ls, mode, analysis, sym, stream);
     if (!gwork) return cudaErrorInvalidValue;
     return mid::launch_gw<4, 4096, 1, SFEM_MID_C2_TH>(t, ls, mode, analysis, sym, gwork, stream);
   }

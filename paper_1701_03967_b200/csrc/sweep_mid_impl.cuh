@@ -68,15 +68,31 @@ template <int NN, int K, int BB, int TH, bool ROWS_, bool GW = false>
 struct Cfg {
   static constexpr int n = NN, m = NN - 1, half = m / 2, ne = NN / 2, N = K, L = NN * K - 1;
   static constexpr bool ROWS = ROWS_;
-  static constexpr int LP = L | 1;
-  static constexpr int PSTR = ROWS ? 1 : BB;  // position stride in the tile
-  __device__ __forceinline__ static constexpr int ix(int pos, int b) { return ROWS ? b * LP + pos : pos * BB + b; }
+  // PAD (one-line tiles): lanes run ALONG the line, at strides of n or 2n
+  // doubles (fills, posts, mixes), i.e. onto 2-4 bank pairs; one pad double
+  // per 16 positions spreads 16 consecutive elements / frequencies over all
+  // 16 bank pairs (C2: shared wavefronts 52M -> ideal 8M in the forward fill).
+  static constexpr bool PAD = BB == 1 && !GW;
+  static constexpr int LP = PAD ? ((L + (L >> 4) + 1) | 1) : (L | 1);
+  static constexpr int PSTR = ROWS ? 1 : BB;  // position stride in the tile (not with PAD: use ix)
+  __device__ __forceinline__ static constexpr int ix(int pos, int b) {
+    return PAD ? pos + (pos >> 4) : (ROWS ? b * LP + pos : pos * BB + b);
+  }
   static constexpr int B = BB, Bh = (BB + 1) / 2, Bm = (m & 1) ? Bh : 0;
   static constexpr int NPAIR = B * half;
-  static constexpr int J = NPAIR + Bm + 2 * Bh;
+  // PK (one-line tiles, m odd; C2's n = 4, K = 4096): the middle job's second
+  // line is a phantom, so its imaginary part carries the line's nodal values
+  // instead and yields the even-index half of the nodal DST-I (forward: X_2k'
+  // = (Re Z_k' - Re Z_{N-k'}) / 2; inverse: the antisymmetrised slots
+  // (s_t - s_{N-t}) / 2 ride in the real part and come back as Im u_k').  Only
+  // the odd-index nodal job remains: J = half + 2 jobs instead of half + 3, which
+  // is what lets a K = 4096 line's FFT work fit in shared memory (192 KB).
+  static constexpr bool PK = !GW && BB == 1 && (m & 1) != 0;
+  static constexpr int ND = PK ? 1 : 2 * Bh;  // nodal jobs
+  static constexpr int J = NPAIR + Bm + ND;
   static constexpr int THREADS = TH;
   static constexpr int WD = 2 * J * K;  // FFT buffer (doubles)
-  static constexpr int TD = (ROWS ? LP : L) * B;  // tile (doubles)
+  static constexpr int TD = ((ROWS || PAD) ? LP : L) * B;  // tile (doubles)
   static constexpr int REGION = (GW || TD > WD) ? TD : WD;  // GW: FFT work in global scratch
   static constexpr int NCEN = m * B;  // centre sums
   static constexpr int CHUNKS = NCEN > 0 ? (TH / NCEN > 0 ? TH / NCEN : 1) : 1;
@@ -380,7 +396,7 @@ __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) 
 // consecutive W entries of one index: conflict-free).
 template <class C, int NT>
 __device__ __forceinline__ void item_job(int it, int& job, int& t) {
-  constexpr int NP = C::NPAIR, NM = C::Bm, ND = 2 * C::Bh;
+  constexpr int NP = C::NPAIR, NM = C::Bm, ND = C::ND;
   constexpr int P = NP * NT, PM = (NP + NM) * NT;
   if (NP > 0 && it < P) {
     job = it % (NP > 0 ? NP : 1);
@@ -486,10 +502,11 @@ __device__ __forceinline__ void forward_fill(const double* T, double* R, double*
           g1 = -g1;
           g2 = -g2;
         }
+        if (C::PK) g2 = tt > 0 ? T[C::ix(tt * n - 1, b)] : 0.0;  // nodal values (even-index DST-I half)
         z[i] = make_double2(g1, g2);
       } else {
         const int jb = job - NPAIR - C::Bm;
-        const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+        const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, b2 = b + Bh;
         if (tt > 0) {
           z[i] = make_double2(T[C::ix(tt * n - 1, b)], b2 < B ? T[C::ix(tt * n - 1, b2)] : 0.0);
           if (which) z[i] = c_mul(z[i], __ldg(om + tt));
@@ -567,10 +584,16 @@ __device__ __forceinline__ Out2 forward_post_item(const double2* Z, int it, cons
       const int b = job - NPAIR, bb = b + Bh;
       o.i1 = C::ix(m + (N - k - 1) * n + 1 + C::half, b);
       if (bb < B) o.i2 = C::ix(m + (N - k - 1) * n + 1 + C::half, bb);
+      if (C::PK && (k & 1) == 0) {
+        // even nodal frequency k = 2 kp from the imaginary payload
+        const int kp = k / 2;
+        o.v2 = 0.5 * (Z[kp * J + job].x - Z[(N - kp) * J + job].x);
+        o.i2 = C::ix(m + (k - 1) * n, b);
+      }
     }
   } else {
     const int jb = job - NPAIR - C::Bm;
-    const int b = jb % Bh, which = jb / Bh, bb = b + Bh;
+    const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, bb = b + Bh;
     if ((k & 1) == which) {
       double2 d;
       if (!which) {
@@ -682,7 +705,7 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
       for (int g = 0; g < G; ++g) {
         const double* pin = Tin + C::ix(m + (k - 1) * n, b0 + g);
 #pragma unroll
-        for (int s = 0; s < n; ++s) v[g][s] = pin[s * C::PSTR];
+        for (int s = 0; s < n; ++s) v[g][s] = C::PAD ? Tin[C::ix(m + (k - 1) * n + s, b0 + g)] : pin[s * C::PSTR];
       }
       if (MODE != kInverse) {
 #if SFEM_MID_KMIX
@@ -744,14 +767,14 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 #endif
           double* p = T + C::ix(m + (k - 1) * n, b0 + g);
 #pragma unroll
-          for (int s = 0; s < n; ++s) p[s * C::PSTR] = v[g][s];
+          for (int s = 0; s < n; ++s) (C::PAD ? T[C::ix(m + (k - 1) * n + s, b0 + g)] : p[s * C::PSTR]) = v[g][s];
         }
       } else {
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           double* p = T + C::ix(m + (k - 1) * n, b0 + g);
 #pragma unroll
-          for (int l = 0; l < n; ++l) p[l * C::PSTR] = c[g][l];
+          for (int l = 0; l < n; ++l) (C::PAD ? T[C::ix(m + (k - 1) * n + l, b0 + g)] : p[l * C::PSTR]) = c[g][l];
         }
       }
     } else if (m > 0) {
@@ -821,9 +844,14 @@ __device__ __forceinline__ double2 inverse_fill_item(const double* T, int it, in
       const double2 v2 = c_mul(w, make_double2(bx, -br));
       // conj(V1 + i V2): the inverse DFT runs as a forward FFT of the conjugate
       z = make_double2(v1.x - v2.y, -(v1.y + v2.x));
+      if (C::PK && job >= NPAIR) {
+        // + (s_t - s_{N-t}) / 2 (antisymmetric, real): its inverse DFT is i * sum_t s_t sin(2 pi t j / N)
+        const int b = job - NPAIR;
+        z.x += 0.5 * (T[C::ix(m + (tt - 1) * n, b)] - T[C::ix(m + (N - tt - 1) * n, b)]);
+      }
     } else {
       const int jb = job - NPAIR - C::Bm;
-      const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+      const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, b2 = b + Bh;
       z = make_double2(T[C::ix(m + (tt - 1) * n, b)], b2 < B ? T[C::ix(m + (tt - 1) * n, b2)] : 0.0);
       if (which) z = c_mul(z, __ldg(om + tt));
     }
@@ -892,10 +920,14 @@ __device__ __forceinline__ Out2 inverse_post_item(const double2* Z, int it, cons
         o.v2 = c2 + (odd ? -uim : uim);
         o.i2 = C::ix(e * n + hc, b2);
       }
+      if (C::PK && tt >= 1 && 2 * tt <= N - 1) {
+        o.v2 = uim;  // node 2 tt
+        o.i2 = C::ix(2 * tt * n - 1, b);
+      }
     }
   } else {
     const int jb = job - NPAIR - C::Bm;
-    const int b = jb % Bh, which = jb / Bh, b2 = b + Bh;
+    const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, b2 = b + Bh;
     const int j = tt;
     if (j >= 1 && j <= N - 1 && (j & 1) == which) {
       double2 d;
@@ -1010,7 +1042,7 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
   } else {
     for (int it = threadIdx.x; it < L * B; it += TH) {
       const int pos = it / B, b = it % B;
-      cp_async8(R + it, ls.src + off[b] + pos * ps, b < Bv);
+      cp_async8(R + C::ix(pos, b), ls.src + off[b] + pos * ps, b < Bv);
     }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -1048,7 +1080,7 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
   } else {
     for (int it = threadIdx.x; it < L * B; it += TH) {
       const int pos = it / B, b = it % B;
-      if (b < Bv) ls.dst[off[b] + pos * ps] = R[it];
+      if (b < Bv) ls.dst[off[b] + pos * ps] = R[C::ix(pos, b)];
     }
   }
   SFEM_PT(5);
