@@ -126,11 +126,27 @@ void upload_table(sfem_table_s* t) {
                                                    &d.e0_fwd_d,  &d.e0_inv,    &d.eig,     &d.tw,
                                                    &d.mk,        &d.mkh,       &d.om,
                                                    &d.mixT_w,    &d.mixT_d,    &d.mixT_i,    &d.nsq};
+  // k-contiguous per-(l, k) copies of the eigenvalues and norms (coefficient
+  // order m + (k-1) n + l -> [l][k]): lanes over consecutive k read one line
+  std::vector<double> eigT(static_cast<size_t>(d.n) * d.K, 0.0), nsqT(static_cast<size_t>(d.n) * d.K, 1.0);
+  for (int k = 1; k < d.K; ++k)
+    for (int l = 0; l < d.n; ++l) {
+      eigT[static_cast<size_t>(l) * d.K + k] = d.eig[(d.n - 1) + static_cast<size_t>(k - 1) * d.n + l];
+      nsqT[static_cast<size_t>(l) * d.K + k] = d.nsq[(d.n - 1) + static_cast<size_t>(k - 1) * d.n + l];
+    }
+  parts.push_back(&eigT);
+  parts.push_back(&nsqT);
   std::vector<size_t> offs;
   size_t total = 0;
-  for (const auto* p : parts) {
+  for (size_t i = 0; i < parts.size(); ++i) {
+    // the k-contiguous arrays (index k >= 1 used) start one double before a
+    // 128-byte boundary: a warp's 16 consecutive frequencies k = 1 + 16 j ..
+    // are one aligned line (two L1 tag requests per load otherwise)
+    const bool kcont = i >= 11 && i != 14;
+    if (kcont) total = ((total + 1 + 15) & ~static_cast<size_t>(15)) - 1;
     offs.push_back(total);
-    total += (p->size() + 1) & ~static_cast<size_t>(1);  // keep 16-byte alignment
+    total += (parts[i]->size() + 1) & ~static_cast<size_t>(1);  // keep 16-byte alignment
+    if (kcont) total = (total + 1) & ~static_cast<size_t>(1);
   }
   std::vector<double> packed(total, 0.0);
   for (size_t i = 0; i < parts.size(); ++i)
@@ -160,6 +176,8 @@ void upload_table(sfem_table_s* t) {
   v.mixT_d = t->dbuf + offs[12];
   v.mixT_i = t->dbuf + offs[13];
   v.nsq = t->dbuf + offs[14];
+  v.eigT = t->dbuf + offs[15];
+  v.nsqT = t->dbuf + offs[16];
   const std::vector<int> r = factor_radices(d.K);
   require(static_cast<int>(r.size()) <= kMaxPasses, "table: too many FFT passes");
   v.npass = static_cast<int>(r.size());

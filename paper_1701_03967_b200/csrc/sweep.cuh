@@ -24,6 +24,8 @@ struct DevTable {
   const double* mixT_w;     // n x n x K, [l][s][k] (k-contiguous copies of mix_fwd_w; k = 0 unused)
   const double* mixT_d;     // same for mix_fwd_d
   const double* mixT_i;     // n x n x K, [s][l][k] copy of mix_inv
+  const double* eigT;       // n x K, [l][k]: eig[m + (k-1) n + l] (k = 0 unused)
+  const double* nsqT;       // n x K, [l][k]: nsq[m + (k-1) n + l]
   const double2* tw;        // N: exp(-2 pi i t/N)
   const double2* mk;        // N: exp(-i pi k/(2N))
   const double2* mkh;       // N: 0.5 exp(+i pi k/(2N))

@@ -33,8 +33,12 @@
 #include "fft_reg.cuh"
 #include "sweep.cuh"
 
+// Resident CTAs per SM asked of ptxas: 3 (128 registers) for n >= 6; 4 (96
+// registers) for n <= 5, whose mix items hold fewer values (measured
+// profiles/r2l_rows_ab.txt: n = 2 / 4 / 5 fused sweeps -12 / -6 / -7 %, n = 9
+// +75 % from spills).
 #ifndef SFEM_ROWS_MINB
-#define SFEM_ROWS_MINB 3
+#define SFEM_ROWS_MINB(NN) ((NN) <= 5 ? 4 : 3)
 #endif
 
 namespace sfem_b200 {
@@ -184,10 +188,19 @@ struct Unroll {
 // entries, and keeping the forward loads live for the inverse costs 2 x n^2
 // registers.
 __device__ __forceinline__ double ldg_once(const double* p) {
+#ifdef SFEM_ROWS_LDG_PLAIN
+  return __ldg(p);
+#else
   double v;
   asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
+#endif
 }
+#ifdef SFEM_ROWS_NOFENCE
+#define SFEM_ROWS_FENCE()
+#else
+#define SFEM_ROWS_FENCE() asm volatile("" ::: "memory")
+#endif
 
 // Shared-memory load the compiler may not replace by the value it just
 // stored there (the mix parks its coefficients in smem to free registers).
@@ -608,11 +621,10 @@ __device__ __forceinline__ void mix_item(int item, double* X, const double* __re
 #pragma unroll
       for (int bb = 0; bb < 4; ++bb) acc[bb] = fma(mv, vv[s][bb], acc[bb]);
     }
-    const int pos = M + (k - 1) * NN + l;
-    const double lam = f_last * __ldg(eig + pos), ns = __ldg(nsq + pos);
+    const double lam = f_last * __ldg(eig + l * N + k), ns = __ldg(nsq + l * N + k);  // eigT / nsqT ([l][k])
 #pragma unroll
     for (int bb = 0; bb < 4; ++bb) at(L_, bb) = sym_div(acc[bb], (bs[bb] + lam) * ns);
-    asm volatile("" ::: "memory");  // one column of matrix loads in flight at a time (register budget)
+    SFEM_ROWS_FENCE();  // one column of matrix loads in flight at a time (register budget)
   });
 #ifdef SFEM_ROWS_DIAG_FWDONLY
   return;
@@ -635,7 +647,7 @@ __device__ __forceinline__ void mix_item(int item, double* X, const double* __re
     }
 #pragma unroll
     for (int bb = 0; bb < 4; ++bb) at(S_, bb) = acc[bb];
-    asm volatile("" ::: "memory");
+    SFEM_ROWS_FENCE();
   });
 }
 
@@ -672,7 +684,7 @@ __device__ __forceinline__ void mix_zero(int b, const double* C0, double* CI, co
 }
 
 template <int NN>
-__global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB)
+__global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB(NN))
     sweep_rows_fused(DevTable t, double* data, RowSegs segs, long long nrows, SymbolInfo sym,
                      const double* __restrict__ e0F) {
   using C = Cfg<NN>;
@@ -740,7 +752,7 @@ __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB)
   __syncthreads();                              // (B2) S rows and centre partials complete
 #ifndef SFEM_ROWS_DIAG_NOMIX
   if (tid < C::ITEMS) {
-    if ((tid & 15) + 16 * (tid >> 5) < N - 1) mix_item<NN>(tid, T, t.mixT_i, t.eig, t.nsq, base, sym.f_last);
+    if ((tid & 15) + 16 * (tid >> 5) < N - 1) mix_item<NN>(tid, T, t.mixT_i, t.eigT, t.nsqT, base, sym.f_last);
   }
 #else
   if (false) {
