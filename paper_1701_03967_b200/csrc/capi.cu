@@ -218,6 +218,7 @@ struct Step {
   // TMA description (strided steps): tensor map for the data pointer it was
   // encoded for, re-encoded when the pointer changes.
   bool tma = false;
+  bool mid_tma = false;    // sweep_mid_tma (tile of box[0] lines)
   bool bulk_rows = false;  // fused last-axis sweep with per-row bulk copies
   TmaGeom geo{};
   cuuint64_t dims[4] = {1, 1, 1, 1}, strides[3] = {0, 0, 0};
@@ -378,6 +379,35 @@ Step strided_step(const View& v, int a, int mode) {
     s.geo.ext0 = v.ext[N - 1];
     s.geo.ext2 = static_cast<long long>(s.dims[2]);
     s.geo.ntiles = s.geo.nblk0 * static_cast<long long>(s.dims[2]) * static_cast<long long>(s.dims[3]);
+  } else if (v.use_fast && mid_tma_lines(dt.n, dt.K) > 0 && (v.pitch * 8) % 16 == 0 && v.ext[N - 1] >= 2) {
+    // mid kernels: the same 4-D view, tiles of `tb` last-axis indices
+    const int tb = mid_tma_lines(dt.n, dt.K);
+    s.mid_tma = true;
+    long long total_bytes = 8 * v.rows() * v.pitch;
+    total_bytes = (total_bytes + 15) & ~15LL;
+    s.dims[0] = v.ext[N - 1];
+    s.dims[1] = v.ext[a];
+    s.strides[0] = st[a] * 8;
+    s.strides[1] = s.strides[2] = total_bytes;
+    if (outer.size() >= 1) {
+      s.dims[2] = v.ext[outer.back()];
+      s.strides[1] = st[outer.back()] * 8;
+    }
+    if (outer.size() == 2) {
+      s.dims[3] = v.ext[outer[0]];
+      s.strides[2] = st[outer[0]] * 8;
+    }
+    s.geo.nbox = static_cast<int>((v.ext[a] + 255) / 256);
+    s.geo.boxp = static_cast<int>((v.ext[a] + s.geo.nbox - 1) / s.geo.nbox);
+    const int balign = std::max(1, 16 / tb);  // boxes start 128-byte aligned in shared memory
+    s.geo.boxp = (s.geo.boxp + balign - 1) / balign * balign;
+    s.geo.nblk0 = (v.ext[N - 1] + tb - 1) / tb;
+    s.geo.ext0 = v.ext[N - 1];
+    s.geo.ext2 = static_cast<long long>(s.dims[2]);
+    s.geo.ntiles = s.geo.nblk0 * static_cast<long long>(s.dims[2]) * static_cast<long long>(s.dims[3]);
+    s.box[0] = static_cast<cuuint32_t>(tb);
+    s.box[1] = static_cast<cuuint32_t>(s.geo.boxp);
+    s.box[2] = s.box[3] = 1;
   }
   return s;
 }
@@ -452,6 +482,9 @@ void launch_steps(std::vector<Step>& steps, double* user, sfem_ctx ctx, cudaStre
     } else if (s.tma && aligned) {
       encode_map(s, data);
       ck(launch_sweep_tma(dt, &s.map, nullptr, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
+    } else if (s.mid_tma && aligned) {
+      encode_map(s, data);
+      ck(launch_sweep_mid_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "mid tma sweep launch");
     } else if (s.bulk_rows && aligned) {
       RowSegs rs{};
       rs.n = 1;

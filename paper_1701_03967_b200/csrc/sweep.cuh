@@ -171,6 +171,13 @@ bool has_mid_sweep(int n, int K);
 size_t mid_work_doubles(int n, int K, long long nlines);
 cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& lines, int mode, int analysis,
                              const SymbolInfo* sym, cudaStream_t stream, double* gwork = nullptr);
+// Strided mid-kernel sweeps with TMA tiles (the tuned shapes): lines per tile
+// (0: no TMA kernel for this table) and the launch.  `tmap`: 4-D tensor map
+// {last axis, swept axis, outer, outer} with box {lines, geo.boxp, 1, 1};
+// geo.nblk0 counts tiles of `lines` last-axis indices.  In place.
+int mid_tma_lines(int n, int K);
+cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
+                                 cudaStream_t stream);
 
 // Slot-major class tiles (nodal (K+1) x count, interior K*(n-1) x count,
 // [j*count + b]) <-> the slot-major dof tile (n*K-1) x count (lines_block.cu).

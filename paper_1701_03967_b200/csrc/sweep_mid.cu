@@ -120,6 +120,41 @@ bool mid_auto(int n, int K) {
 #endif
 }
 
+// Strided sweeps of the tuned shapes move their tiles by TMA (sweep_mid_tma);
+// SFEM_MID_TMA=0 keeps the cp.async kernels (A/B).
+static bool mid_tma_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SFEM_MID_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+int mid_tma_lines(int n, int K) {
+  if (!mid_tma_enabled()) return 0;
+  if (n == 1 && K == 1024) return SFEM_MID_B_N1;
+  if (n == 2 && K == 512) return SFEM_MID_B_N2;
+  if (n == 4 && K == 256) return SFEM_MID_B_N4;
+  if (n == 9 && K == 114) return SFEM_MID_B_N9;
+  if (n == 9 && K == 1024) return 2;
+  return 0;
+}
+
+cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
+                                 cudaStream_t stream) {
+  if (geo.ntiles <= 0) return cudaSuccess;
+  if (t.n == 1 && t.K == 1024)
+    return mid::launch_tma<1, 1024, SFEM_MID_B_N1, SFEM_MID_TH_N1>(t, tmap, geo, mode, analysis, stream);
+  if (t.n == 2 && t.K == 512)
+    return mid::launch_tma<2, 512, SFEM_MID_B_N2, SFEM_MID_TH_N2>(t, tmap, geo, mode, analysis, stream);
+  if (t.n == 4 && t.K == 256)
+    return mid::launch_tma<4, 256, SFEM_MID_B_N4, SFEM_MID_TH_N4>(t, tmap, geo, mode, analysis, stream);
+  if (t.n == 9 && t.K == 114)
+    return mid::launch_tma<9, 114, SFEM_MID_B_N9, SFEM_MID_TH_N9>(t, tmap, geo, mode, analysis, stream);
+  if (t.n == 9 && t.K == 1024) return mid::launch_tma<9, 1024, 2, SFEM_MID_C3_TH>(t, tmap, geo, mode, analysis, stream);
+  return cudaErrorNotSupported;
+}
+
 bool has_mid_sweep(int n, int K) {
   return (n == 1 && K == 1024) || (n == 2 && K == 512) || (n == 4 && K == 256) || (n == 9 && K == 114) ||
          (n == 9 && K == 1024) || (n == 4 && K == 4096) || mid_auto(n, K);

@@ -20,6 +20,7 @@
 //     all threads and reduced in a fixed order (deterministic).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -1087,6 +1088,151 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
   SFEM_PT_FLUSH(20 + MODE);
 }
 
+
+// ---------------------------------------------------------------------------
+// Strided sweeps with the tile moved by TMA (same stages as sweep_mid, same
+// dense tile layout T[pos][b]): the tensor is viewed as 4-D {last axis, swept
+// axis, outer axes} (TmaGeom, sweep.cuh); a tile is BB consecutive last-axis
+// indices x all positions at one (c2, c3), brought in by nbox box copies
+// {BB, boxp} issued by one thread and signalled on an mbarrier, and written
+// back by nbox tensor stores.  Lines / positions outside the tensor are
+// zero-filled on load and clipped on store by the TMA unit, so partial tiles
+// need no per-line bookkeeping.  Replaces 2 x L*BB/2 16-byte cp.async / store
+// instructions per tile (a quarter of the kernel's instructions at C5 n = 4).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned mid_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int NN, int K, int BB, int TH>
+struct TmaShape {
+  using C = Cfg<NN, K, BB, TH, false>;
+  static constexpr int NBOX = (C::L + 255) / 256;
+  // every box starts 128-byte aligned in shared memory: BOXP * BB a multiple of 16 doubles
+  static constexpr int BALIGN = 16 / BB > 0 ? 16 / BB : 1;
+  static constexpr int BOXP = ((C::L + NBOX - 1) / NBOX + BALIGN - 1) / BALIGN * BALIGN;
+  // the boxes' zero-filled tail rows must fit the region; 16-byte box rows at least
+  static constexpr bool OK = NBOX * BOXP * BB <= C::REGION && (BB * 8) % 16 == 0;
+  // the mbarrier lives behind the regular layout
+  static constexpr int BAR_OFF = (C::TOTAL + 1) & ~1;
+  static constexpr size_t SMEM = static_cast<size_t>(BAR_OFF + 2) * sizeof(double);
+};
+
+template <int NN, int K, int BB, int TH, int MODE>
+__global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)
+    sweep_mid_tma(DevTable t, const __grid_constant__ CUtensorMap tmap, TmaGeom geo, const double* __restrict__ mixF,
+                  const double* __restrict__ e0F) {
+  using C = Cfg<NN, K, BB, TH, false>;
+  using TS = TmaShape<NN, K, BB, TH>;
+  extern __shared__ __align__(128) double smem[];  // no static shared memory: the tile starts 128-byte aligned
+  double* R = smem;
+  double* C0 = smem + C::C0_OFF;
+  double* PS = smem + C::PS_OFF;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + TS::BAR_OFF);
+  SFEM_PT_DECL;
+  SFEM_PT(0);
+  int c0, c2, c3;
+  if (gridDim.y > 1 || gridDim.z > 1 || geo.ntiles == geo.nblk0) {
+    c0 = static_cast<int>(blockIdx.x) * BB;
+    c2 = static_cast<int>(blockIdx.y);
+    c3 = static_cast<int>(blockIdx.z);
+  } else {
+    const long long tile = blockIdx.x;
+    c0 = static_cast<int>(tile % geo.nblk0) * BB;
+    const long long rest = tile / geo.nblk0;
+    c2 = static_cast<int>(rest % geo.ext2);
+    c3 = static_cast<int>(rest / geo.ext2);
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mid_smem_u32(bar)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mid_smem_u32(bar)),
+                 "r"(static_cast<unsigned>(TS::NBOX * TS::BOXP * BB * sizeof(double)))
+                 : "memory");
+#pragma unroll 1
+    for (int j = 0; j < TS::NBOX; ++j)
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+          "[%6];\n" ::"r"(mid_smem_u32(R + j * TS::BOXP * BB)),
+          "l"(&tmap), "r"(c0), "r"(j * TS::BOXP), "r"(c2), "r"(c3), "r"(mid_smem_u32(bar))
+          : "memory");
+  }
+  __syncthreads();  // the barrier is initialised before anyone polls it
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(mid_smem_u32(bar)),
+      "r"(0)
+      : "memory");
+  SFEM_PT(1);
+  SymbolInfo nosym{};
+  if (MODE != kInverse) {
+    forward_fill<C>(R, R, PS, t.om);
+    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    centre_reduce<C>(PS, C0);
+    forward_post<C>(reinterpret_cast<const double2*>(R), R, t.mk);
+  }
+  SFEM_PT(2);
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, nullptr, t.eig, nosym.f_last);
+  SFEM_PT(3);
+  if (MODE != kForward) {
+    inverse_fill<C>(R, reinterpret_cast<double2*>(R), t.mkh, t.om);
+    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    inverse_post<C>(reinterpret_cast<const double2*>(R), R, C0);
+  }
+  SFEM_PT(4);
+  // every stage above ends with a block barrier; make the generic-proxy
+  // writes of the tile visible to the async proxy before the tensor stores
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int j = 0; j < TS::NBOX; ++j)
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(&tmap),
+                   "r"(c0), "r"(j * TS::BOXP), "r"(c2), "r"(c3), "r"(mid_smem_u32(R + j * TS::BOXP * BB))
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  }
+  SFEM_PT(5);
+  SFEM_PT_FLUSH(30 + MODE);
+}
+
+template <int NN, int K, int BB, int TH>
+cudaError_t launch_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
+                       cudaStream_t stream) {
+  using TS = TmaShape<NN, K, BB, TH>;
+  if constexpr (!TS::OK) {
+    return cudaErrorNotSupported;
+  } else {
+    if (mode == kForwardDivideInverse || geo.nbox != TS::NBOX || geo.boxp != TS::BOXP) return cudaErrorInvalidValue;
+    const double* mixF = SFEM_MID_KMIX ? (analysis == kDirect ? t.mixT_d : t.mixT_w)
+                                       : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
+    const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
+    const CUtensorMap* map = static_cast<const CUtensorMap*>(tmap);
+    const long long ext3 = geo.ntiles / (geo.nblk0 * geo.ext2);
+    const bool grid3 = geo.nblk0 < (1LL << 31) && geo.ext2 <= 65535 && ext3 <= 65535;
+    const dim3 grid = grid3 ? dim3(static_cast<unsigned>(geo.nblk0), static_cast<unsigned>(geo.ext2),
+                                   static_cast<unsigned>(ext3))
+                            : dim3(static_cast<unsigned>(geo.ntiles));
+    cudaError_t err;
+    if (mode == kForward) {
+      auto kern = sweep_mid_tma<NN, K, BB, TH, kForward>;
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TS::SMEM));
+      if (err != cudaSuccess) return err;
+      kern<<<grid, TH, TS::SMEM, stream>>>(t, *map, geo, mixF, e0F);
+    } else {
+      auto kern = sweep_mid_tma<NN, K, BB, TH, kInverse>;
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TS::SMEM));
+      if (err != cudaSuccess) return err;
+      kern<<<grid, TH, TS::SMEM, stream>>>(t, *map, geo, mixF, e0F);
+    }
+    return cudaGetLastError();
+  }
+}
 
 // Lines too long for an FFT buffer in shared memory (C2: n=4, K=4096): the
 // tile stays in shared memory, the J*K complex FFT work of the CTA lives in
