@@ -54,6 +54,9 @@
 #ifndef SFEM_MID_MIXG
 #define SFEM_MID_MIXG 4
 #endif
+#ifndef SFEM_MID_ROWS_BULK
+#define SFEM_MID_ROWS_BULK 1
+#endif
 
 namespace sfem_b200 {
 namespace mid {
@@ -74,7 +77,13 @@ struct Cfg {
   // per 16 positions spreads 16 consecutive elements / frequencies over all
   // 16 bank pairs (C2: shared wavefronts 52M -> ideal 8M in the forward fill).
   static constexpr bool PAD = BB == 1 && !GW;
-  static constexpr int LP = PAD ? ((L + (L >> 4) + 1) | 1) : (L | 1);
+  // Row tiles of B > 1 lines: rows move as one bulk copy each (cp.async.bulk,
+  // 16-byte aligned, L rounded up to even doubles), so the row pitch is even:
+  // 2 mod 16 doubles keeps the 8 lines of a tile on 8 different bank pairs.
+  // (SFEM_MID_ROWS_BULK=0: odd pitch and 8-byte cp.async copies.)
+  static constexpr bool BULK = SFEM_MID_ROWS_BULK && ROWS_ && BB > 1 && !GW;
+  static constexpr int LB = (L + 1) & ~1;  // doubles per bulk row copy
+  static constexpr int LP = PAD ? ((L + (L >> 4) + 1) | 1) : (BULK ? ((LB + 15) / 16 * 16 + 2) : (L | 1));
   static constexpr int PSTR = ROWS ? 1 : BB;  // position stride in the tile (not with PAD: use ix)
   __device__ __forceinline__ static constexpr int ix(int pos, int b) {
     return PAD ? pos + (pos >> 4) : (ROWS ? b * LP + pos : pos * BB + b);
@@ -957,6 +966,10 @@ __device__ __forceinline__ void inverse_post(const double2* Z, double* R, const 
 }
 
 // ------------------------------------------------------------ kernel
+__device__ __forceinline__ unsigned mid_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
@@ -987,7 +1000,7 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
               const double* __restrict__ e0F) {
   using C = Cfg<NN, K, BB, TH, ROWS>;
   constexpr int B = C::B, L = C::L;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   double* R = smem;
   double* C0 = smem + C::C0_OFF;
   double* PS = smem + C::PS_OFF;
@@ -1028,10 +1041,52 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
   // tile load, all copies in flight at once (phantom lines zero-filled)
   const long long ps = ls.ps;
   const bool vec = vec_tile<C>(off, Bv, ps, ls.src, ls.dst);
-  if (ROWS) {
-    for (int it = threadIdx.x; it < L * B; it += TH) {
-      const int b = it / L, pos = it - b * L;
-      cp_async8(R + C::ix(pos, b), ls.src + off[b] + pos, b < Bv);
+  // rows as bulk copies: 16-byte aligned rows with room for the even length
+  __shared__ unsigned long long rowbar;
+  bool bulk = false;
+  if constexpr (C::BULK) {
+    bulk = ((reinterpret_cast<unsigned long long>(ls.src) | reinterpret_cast<unsigned long long>(ls.dst)) & 15) == 0 &&
+           ((ls.os1 | ls.os2 | ls.is) & 1) == 0 && (ls.nlines == 1 || C::LB <= (ls.ninner > 1 ? ls.is : ls.os1));
+  }
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mid_smem_u32(&rowbar)), "r"(1) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mid_smem_u32(&rowbar)),
+                   "r"(static_cast<unsigned>(Bv * C::LB * sizeof(double)))
+                   : "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x < Bv)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       mid_smem_u32(R + C::ix(0, threadIdx.x))),
+                   "l"(ls.src + off[threadIdx.x]), "r"(static_cast<unsigned>(C::LB * sizeof(double))),
+                   "r"(mid_smem_u32(&rowbar))
+                   : "memory");
+    for (int it = threadIdx.x; it < (B - Bv) * C::LP; it += TH) R[Bv * C::LP + it] = 0.0;  // phantom rows
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(mid_smem_u32(&rowbar)),
+        "r"(0)
+        : "memory");
+  } else if (ROWS) {
+    // row by row: the inner loop is one add per element (a flat index costs a
+    // division and an offset lookup per 8-byte copy)
+#pragma unroll 1
+    for (int b = 0; b < B; ++b) {
+      const double* src = ls.src + off[b];
+      double* dstrow = R + C::ix(0, b);
+      const bool ok = b < Bv;
+      if (C::PAD) {
+        for (int pos = threadIdx.x; pos < L; pos += TH) cp_async8(R + C::ix(pos, b), src + pos, ok);
+      } else {
+#pragma unroll 4
+        for (int pos = threadIdx.x; pos < L; pos += TH) cp_async8(dstrow + pos, src + pos, ok);
+      }
     }
   } else if (vec) {
     constexpr int B2 = B / 2;
@@ -1066,10 +1121,28 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
   }
   SFEM_PT(4);
 
-  if (ROWS) {
-    for (int it = threadIdx.x; it < L * B; it += TH) {
-      const int b = it / L, pos = it - b * L;
-      if (b < Bv) ls.dst[off[b] + pos] = R[C::ix(pos, b)];
+  if (bulk) {
+    if (C::LB > L && threadIdx.x < B) R[C::ix(L, threadIdx.x)] = 0.0;  // the row's pad element
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < Bv) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(ls.dst + off[threadIdx.x]),
+                   "r"(mid_smem_u32(R + C::ix(0, threadIdx.x))), "r"(static_cast<unsigned>(C::LB * sizeof(double)))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+  } else if (ROWS) {
+#pragma unroll 1
+    for (int b = 0; b < Bv; ++b) {
+      double* dst = ls.dst + off[b];
+      const double* srow = R + C::ix(0, b);
+      if (C::PAD) {
+        for (int pos = threadIdx.x; pos < L; pos += TH) dst[pos] = R[C::ix(pos, b)];
+      } else {
+#pragma unroll 4
+        for (int pos = threadIdx.x; pos < L; pos += TH) dst[pos] = srow[pos];
+      }
     }
   } else if (vec) {
     constexpr int B2 = B / 2;
@@ -1100,10 +1173,6 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 regis
 // need no per-line bookkeeping.  Replaces 2 x L*BB/2 16-byte cp.async / store
 // instructions per tile (a quarter of the kernel's instructions at C5 n = 4).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned mid_smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
 template <int NN, int K, int BB, int TH>
 struct TmaShape {
   using C = Cfg<NN, K, BB, TH, false>;
