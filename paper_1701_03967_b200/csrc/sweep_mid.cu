@@ -66,14 +66,17 @@ extern template cudaError_t launch_auto_n<1000>(const DevTable&, const LineSet&,
 #ifndef SFEM_MID_B_N2
 #define SFEM_MID_B_N2 8
 #endif
+// Threads: one radix-16 / radix-8 butterfly per thread and pass (J * K / R
+// items), so a pass keeps R complex values per thread, not 2R (spills):
+// n = 2: J = 12 jobs x 512 / 8 = 768 items = 2 x 384; n = 4: 20 x 256 / 16 = 320.
 #ifndef SFEM_MID_TH_N2
-#define SFEM_MID_TH_N2 256
+#define SFEM_MID_TH_N2 384
 #endif
 #ifndef SFEM_MID_B_N4
 #define SFEM_MID_B_N4 8
 #endif
 #ifndef SFEM_MID_TH_N4
-#define SFEM_MID_TH_N4 256
+#define SFEM_MID_TH_N4 320
 #endif
 #ifndef SFEM_MID_B_N9
 #define SFEM_MID_B_N9 8

@@ -39,8 +39,9 @@
 #ifndef SFEM_MID_C2_TH
 #define SFEM_MID_C2_TH 512
 #endif
+// C3 (n = 9, K = 1024, two lines: J = 10 jobs): 10 x 1024 / 16 = 640 radix-16 items
 #ifndef SFEM_MID_C3_TH
-#define SFEM_MID_C3_TH 512
+#define SFEM_MID_C3_TH 640
 #endif
 #ifndef SFEM_MID_KMIX
 #define SFEM_MID_KMIX 1
@@ -634,18 +635,31 @@ __device__ __forceinline__ void run_out2(double* R, F f) {
       if (o.i2 >= 0) R[o.i2] = o.v2;
     }
   } else {
+    // Only the values cross the barrier in registers; the target indices are
+    // recomputed afterwards (f is called again and only its index part is
+    // used, so its loads are dead): 4 registers per item instead of 6, which
+    // is what spilled in the 20-items-per-thread tiles.
     constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
-    Out2 o[IPT];
+    double v1[IPT], v2[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const int it = threadIdx.x + i * C::THREADS;
-      o[i] = it < ITEMS ? f(it) : Out2{0.0, 0.0, -1, -1};
+      v1[i] = v2[i] = 0.0;
+      if (it < ITEMS) {
+        const Out2 o = f(it);
+        v1[i] = o.v1;
+        v2[i] = o.v2;
+      }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
-      if (o[i].i1 >= 0) R[o[i].i1] = o[i].v1;
-      if (o[i].i2 >= 0) R[o[i].i2] = o[i].v2;
+      const int it = threadIdx.x + i * C::THREADS;
+      if (it < ITEMS) {
+        const Out2 o = f(it);
+        if (o.i1 >= 0) R[o.i1] = v1[i];
+        if (o.i2 >= 0) R[o.i2] = v2[i];
+      }
     }
   }
   __syncthreads();
@@ -883,17 +897,22 @@ __device__ __forceinline__ void inverse_fill(const double* T, double2* W, const 
   } else {
     constexpr int IPT = (C::N * C::J + C::THREADS - 1) / C::THREADS;
     double2 z[IPT];
-    int wi[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const int it = threadIdx.x + i * C::THREADS;
-      wi[i] = -1;
-      if (it < ITEMS) z[i] = inverse_fill_item<C>(T, it, wi[i], mkh, om);
+      int widx;
+      if (it < ITEMS) z[i] = inverse_fill_item<C>(T, it, widx, mkh, om);
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < IPT; ++i)
-      if (wi[i] >= 0) W[wi[i]] = z[i];
+    for (int i = 0; i < IPT; ++i) {
+      const int it = threadIdx.x + i * C::THREADS;
+      if (it < ITEMS) {
+        int job, tt;
+        item_job<C, C::N>(it, job, tt);
+        W[tt * C::J + job] = z[i];
+      }
+    }
   }
   __syncthreads();
 }
@@ -966,6 +985,10 @@ __device__ __forceinline__ void inverse_post(const double2* Z, double* R, const 
 }
 
 // ------------------------------------------------------------ kernel
+// Resident CTAs per SM asked of ptxas: two for CTAs of up to 384 threads
+// (four / two for 128 / 256), one above.
+__host__ __device__ constexpr int mid_min_blocks(int th) { return th <= 256 ? 512 / th : (th <= 384 ? 2 : 1); }
+
 __device__ __forceinline__ unsigned mid_smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -995,7 +1018,7 @@ __device__ __forceinline__ bool vec_tile(const long long* off, int Bv, long long
 }
 
 template <int NN, int K, int BB, int TH, int MODE, bool ROWS>
-__global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)  // <= 128 registers
+__global__ void __launch_bounds__(TH, mid_min_blocks(TH))  // <= 128 registers
     sweep_mid(DevTable t, LineSet ls, SymbolInfo sym, const double* __restrict__ mixF,
               const double* __restrict__ e0F) {
   using C = Cfg<NN, K, BB, TH, ROWS>;
@@ -1188,7 +1211,7 @@ struct TmaShape {
 };
 
 template <int NN, int K, int BB, int TH, int MODE>
-__global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 512 / TH)
+__global__ void __launch_bounds__(TH, mid_min_blocks(TH))
     sweep_mid_tma(DevTable t, const __grid_constant__ CUtensorMap tmap, TmaGeom geo, const double* __restrict__ mixF,
                   const double* __restrict__ e0F) {
   using C = Cfg<NN, K, BB, TH, false>;
