@@ -57,11 +57,13 @@ extern template cudaError_t launch_auto_n<1000>(const DevTable&, const LineSet&,
 }  // namespace mid
 
 // Lines per tile and threads per CTA of the C5 shapes.
+// n = 1 (K = 1024): four lines (J = 4 jobs, 65 KB) and 256 threads give two
+// CTAs per SM instead of one 131 KB tile (C5 n=1 67.7 -> 64.3 ms)
 #ifndef SFEM_MID_B_N1
-#define SFEM_MID_B_N1 8
+#define SFEM_MID_B_N1 4
 #endif
 #ifndef SFEM_MID_TH_N1
-#define SFEM_MID_TH_N1 512
+#define SFEM_MID_TH_N1 256
 #endif
 #ifndef SFEM_MID_B_N2
 #define SFEM_MID_B_N2 8

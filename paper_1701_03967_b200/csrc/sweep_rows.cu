@@ -85,7 +85,8 @@ struct Cfg {
   static constexpr int BASE_OFF = CI_OFF + MB;
   static constexpr int BAR_OFF = round_up<BASE_OFF + B, 2>();
   static constexpr int TAB_OFF = BAR_OFF + 2;     // tw | mkh | om, N complex each
-  static constexpr int TOTAL_D = TAB_OFF + 6 * N;
+  static constexpr int SOFF_OFF = TAB_OFF + 6 * N;  // S-row offsets [g][slot][4 lines] (ints; rolled mixes)
+  static constexpr int TOTAL_D = SOFF_OFF + (2 * NN * 4 + 1) / 2 + 2;
   static constexpr size_t SMEM = static_cast<size_t>(TOTAL_D) * sizeof(double);
 };
 
@@ -578,6 +579,89 @@ __host__ __device__ constexpr int srow_c(int s, int b) {
   return sbase(j) + (odd ? SR : 0);
 }
 
+// Rolled mixes (SFEM_ROWS_ROLLED_MIX, default): the column loops of the two
+// mixes are real loops (the 9 x 4 FMAs of a column stay unrolled), with the
+// slot offsets of a column's four results read from a small shared table.
+// The unrolled form is ~1800 straight-line instructions executed once per
+// tile and warp; with three CTAs in different phases the fused kernel's 93 KB
+// of code did not stay in the instruction caches (ncu: no_instruction was the
+// top stall reason, 1.2-2.7 per issue).
+#ifndef SFEM_ROWS_ROLLED_MIX
+#define SFEM_ROWS_ROLLED_MIX 1
+#endif
+
+template <int NN>
+__device__ __forceinline__ void mix_item_rolled(int item, double* X, const double* __restrict__ mixT,
+                                                const double* __restrict__ eig, const double* __restrict__ nsq,
+                                                const double* base, double f_last, const int* soff) {
+  using C = Cfg<NN>;
+  const int k = 1 + (item & 15) + 16 * (item >> 5), g = (item >> 4) & 1;
+  constexpr int S_PAIR = C::HALF > 0 ? 1 : (C::MODD ? 1 + C::HALF : 0);
+  constexpr int OG_NOD = srow_c<NN>(0, 4) - srow_c<NN>(0, 0);
+  constexpr int OG_PAIR = srow_c<NN>(S_PAIR, 4) - srow_c<NN>(S_PAIR, 0);
+  constexpr int OG_MID = C::MODD ? srow_c<NN>(1 + C::HALF, 4) - srow_c<NN>(1 + C::HALF, 0) : 0;
+  double* const xn = X + k + g * OG_NOD;
+  double* const xp = X + k + g * OG_PAIR;
+  double* const xm = X + k + g * OG_MID;
+  auto at = [&](auto S_, int bb) -> double& {
+    constexpr int s = decltype(S_)::value;
+    double* const base_ = s == 0 ? xn : ((C::MODD && s == 1 + C::HALF) ? xm : xp);
+    return base_[srow_c<NN>(s, bb)];
+  };
+  double* const Xk = X + k;
+  const int4* so = reinterpret_cast<const int4*>(soff) + g * NN;  // [slot] -> offsets of lines 4g .. 4g+3
+  double vv[NN][4];
+  Unroll<NN>::run([&](auto S_) {
+    constexpr int s = decltype(S_)::value;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) vv[s][bb] = at(S_, bb);
+  });
+  double bs[4];
+#pragma unroll
+  for (int bb = 0; bb < 4; ++bb) bs[bb] = base[4 * g + bb];
+  const double* mk = mixT + k;
+#pragma unroll 1
+  for (int l = 0; l < NN; ++l) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* ml = mk + l * N;
+#pragma unroll
+    for (int s = 0; s < NN; ++s) {
+      const double mv = __ldg(ml + s * NN * N);
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) acc[bb] = fma(mv, vv[s][bb], acc[bb]);
+    }
+    const double lam = f_last * __ldg(eig + l * N + k), ns = __ldg(nsq + l * N + k);
+    const int4 o = so[l];
+    Xk[o.x] = sym_div(acc[0], (bs[0] + lam) * ns);
+    Xk[o.y] = sym_div(acc[1], (bs[1] + lam) * ns);
+    Xk[o.z] = sym_div(acc[2], (bs[2] + lam) * ns);
+    Xk[o.w] = sym_div(acc[3], (bs[3] + lam) * ns);
+  }
+  __threadfence_block();
+  double cv[NN][4];
+  Unroll<NN>::run([&](auto L_) {
+    constexpr int l = decltype(L_)::value;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) cv[l][bb] = lds_once(&at(L_, bb));
+  });
+#pragma unroll 1
+  for (int sI = 0; sI < NN; ++sI) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* ms = mk + sI * NN * N;
+#pragma unroll
+    for (int l = 0; l < NN; ++l) {
+      const double mv = __ldg(ms + l * N);
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) acc[bb] = fma(mv, cv[l][bb], acc[bb]);
+    }
+    const int4 o = so[sI];
+    Xk[o.x] = acc[0];
+    Xk[o.y] = acc[1];
+    Xk[o.z] = acc[2];
+    Xk[o.w] = acc[3];
+  }
+}
+
 template <int NN>
 __device__ __forceinline__ void mix_item(int item, double* X, const double* __restrict__ mixT,
                                          const double* __restrict__ eig, const double* __restrict__ nsq,
@@ -697,6 +781,7 @@ __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB(NN))
   double2* tw = reinterpret_cast<double2*>(smem + C::TAB_OFF);
   double2* mkh = tw + N;
   double2* om = mkh + N;
+  int* soff = reinterpret_cast<int*>(smem + C::SOFF_OFF);
   const int tid = threadIdx.x;
   const long long l0 = static_cast<long long>(blockIdx.x) * B;
   const int Bv = static_cast<int>(min(static_cast<long long>(B), nrows - l0));
@@ -745,6 +830,9 @@ __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB(NN))
     mkh[i] = t.mkh[i];
     om[i] = t.om[i];
   }
+#if SFEM_ROWS_ROLLED_MIX
+  if (tid < 2 * NN * 4) soff[tid] = srow<NN>((tid >> 2) % NN, 4 * (tid / (4 * NN)) + (tid & 3));
+#endif
   __syncthreads();  // tables, bases, phantom rows
   mbar_wait(bar, 0);
   const Job jb = job_of<NN>(tid);
@@ -752,7 +840,13 @@ __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB(NN))
   __syncthreads();                              // (B2) S rows and centre partials complete
 #ifndef SFEM_ROWS_DIAG_NOMIX
   if (tid < C::ITEMS) {
-    if ((tid & 15) + 16 * (tid >> 5) < N - 1) mix_item<NN>(tid, T, t.mixT_i, t.eigT, t.nsqT, base, sym.f_last);
+    // rolled for the large orders only (n = 9: 1.50 -> 1.33 ms; n <= 7: +-2 %, their code is smaller)
+    if ((tid & 15) + 16 * (tid >> 5) < N - 1) {
+      if constexpr (SFEM_ROWS_ROLLED_MIX && NN >= 8)
+        mix_item_rolled<NN>(tid, T, t.mixT_i, t.eigT, t.nsqT, base, sym.f_last, soff);
+      else
+        mix_item<NN>(tid, T, t.mixT_i, t.eigT, t.nsqT, base, sym.f_last);
+    }
   }
 #else
   if (false) {
