@@ -553,6 +553,114 @@ __device__ __forceinline__ void forward_fill(const double* T, double* R, double*
   __syncthreads();
 }
 
+// ---- fill fused into the first pass (in-place kernels) ----------------------
+// The first Stockham pass (NS = 1, no twiddles) reads its butterfly inputs
+// straight from the tile (forward) or the slots (inverse) instead of from a
+// W buffer a separate fill stage wrote: one write and one read of the whole
+// FFT buffer and two block barriers fewer per transform.  Items are grouped by
+// job kind (item_job) so a warp's element code is uniform.
+template <class C>
+__device__ __forceinline__ double2 forward_elem(const double* T, int job, int tt, const double2* __restrict__ om) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, NPAIR = C::NPAIR;
+  double2 z = make_double2(0.0, 0.0);
+  if (job < NPAIR) {
+    const int ii = job / B, b = job % B;
+    const int e = makhoul_src(tt, N);
+    const double ri = T[C::ix(e * n + ii, b)], rr = T[C::ix(e * n + m - 1 - ii, b)];
+    double gg = ri + rr;
+    if (e & 1) gg = -gg;
+    z = make_double2(ri - rr, gg);
+  } else if (job < NPAIR + C::Bm) {
+    const int b = job - NPAIR, b2 = b + Bh;
+    const int e = makhoul_src(tt, N);
+    double g1 = T[C::ix(e * n + C::half, b)];
+    double g2 = b2 < B ? T[C::ix(e * n + C::half, b2)] : 0.0;
+    if (e & 1) {
+      g1 = -g1;
+      g2 = -g2;
+    }
+    if (C::PK) g2 = tt > 0 ? T[C::ix(tt * n - 1, b)] : 0.0;
+    z = make_double2(g1, g2);
+  } else {
+    const int jb = job - NPAIR - C::Bm;
+    const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, b2 = b + Bh;
+    if (tt > 0) {
+      z = make_double2(T[C::ix(tt * n - 1, b)], b2 < B ? T[C::ix(tt * n - 1, b2)] : 0.0);
+      if (which) z = c_mul(z, __ldg(om + tt));
+    }
+  }
+  return z;
+}
+
+template <class C>
+__device__ __forceinline__ void centre_partials(const double* T, double* PS) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B;
+  if constexpr (C::NCEN > 0) {
+    const int cit = threadIdx.x;
+    if (cit < C::CHUNKS * C::NCEN) {
+      const int s = cit % C::NCEN, c = cit / C::NCEN;
+      const int ii = s / B, b = s % B;
+      const int e0 = c * C::ECH, e1 = min(N, e0 + C::ECH);
+      double part = 0.0;
+      for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ix(e * n + m - 1 - ii, b)] : T[C::ix(e * n + ii, b)];
+      PS[cit] = part;
+    }
+  }
+}
+
+// First pass of radix R with element source `elem(job, t)`; W aliases the
+// source, so every thread loads all its inputs before the barrier.
+template <class C, int R, class F>
+__device__ __forceinline__ void fft_pass_first(double2* W, const double2* __restrict__ tw, F elem) {
+  constexpr int N = C::N, J = C::J, NR = N / R, ITEMS = NR * J;
+  constexpr int IPT = (ITEMS + C::THREADS - 1) / C::THREADS;
+  double2 v[IPT][R];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) {
+      int job, j;
+      item_job<C, NR>(it, job, j);
+#pragma unroll
+      for (int q = 0; q < R; ++q) v[i][q] = elem(job, j + q * NR);
+      dft<R, N>(v[i], tw);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int it = threadIdx.x + i * C::THREADS;
+    if (it < ITEMS) {
+      int job, j;
+      item_job<C, NR>(it, job, j);
+#pragma unroll
+      for (int pp = 0; pp < R; ++pp) W[(j * R + pp) * J + job] = v[i][pp];
+    }
+  }
+  __syncthreads();
+}
+
+#ifndef SFEM_MID_FUSED_FILL
+#define SFEM_MID_FUSED_FILL 1
+#endif
+
+// Forward transform of the tile in R (in place): fill + FFT, W = R.
+template <class C>
+__device__ __forceinline__ void forward_fft_inplace(double* R, double* PS, const double2* __restrict__ tw,
+                                                    const double2* __restrict__ om) {
+  using PL = Plan<C::N, few_plan<C>()>;
+  double2* W = reinterpret_cast<double2*>(R);
+  // (not for the one-line tiles of C2: 1.01 -> 1.11 ms there)
+  if constexpr (SFEM_MID_FUSED_FILL && !C::PAD) {
+    centre_partials<C>(R, PS);
+    fft_pass_first<C, PL::R[0]>(W, tw, [&](int job, int t) { return forward_elem<C>(R, job, t, om); });
+    fft<C, 1, PL::R[0]>(W, tw);
+  } else {
+    forward_fill<C>(R, R, PS, om);
+    fft<C>(W, tw);
+  }
+}
+
 // C0[s] = sum over chunks in order.
 template <class C>
 __device__ __forceinline__ void centre_reduce(const double* PS, double* C0) {
@@ -707,7 +815,8 @@ template <class C, int MODE>
 __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, const double* __restrict__ mixF,
                                     const double* __restrict__ e0F, const double* __restrict__ mixI,
                                     const double* __restrict__ e0I, const double* base,
-                                    const double* __restrict__ eig, double f_last) {
+                                    const double* __restrict__ eig, double f_last,
+                                    const double* __restrict__ eigT = nullptr) {
   constexpr int N = C::N, n = C::n, m = C::m, B = C::B;
 #if SFEM_MID_KMIX
 #define MIDX(a, b) (((a) * n + (b)) * N)
@@ -751,7 +860,7 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
             for (int g = 0; g < G; ++g) acc[g] = fma(mv, v[g][s], acc[g]);
           }
           if (MODE == kForwardDivideInverse) {
-            const double ev = __ldg(eig + m + (k - 1) * n + l);
+            const double ev = __ldg(eigT + l * N + k);  // k-contiguous copy: lanes over k read one line
 #pragma unroll
             for (int g = 0; g < G; ++g) acc[g] = mid_div(acc[g], base[b0 + g] + f_last * ev);
           }
@@ -840,13 +949,23 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 
 // ------------------------------------------------------------ inverse fill
 template <class C>
+__device__ __forceinline__ double2 inverse_elem(const double* T, int job, int tt, const double2* __restrict__ mkh,
+                                                const double2* __restrict__ om);
+
+template <class C>
 __device__ __forceinline__ double2 inverse_fill_item(const double* T, int it, int& widx,
                                                      const double2* __restrict__ mkh, const double2* __restrict__ om) {
-  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, J = C::J, NPAIR = C::NPAIR;
-  double2 z = make_double2(0.0, 0.0);
   int job, tt;
-  item_job<C, N>(it, job, tt);
-  widx = tt * J + job;
+  item_job<C, C::N>(it, job, tt);
+  widx = tt * C::J + job;
+  return inverse_elem<C>(T, job, tt, mkh, om);
+}
+
+template <class C>
+__device__ __forceinline__ double2 inverse_elem(const double* T, int job, int tt, const double2* __restrict__ mkh,
+                                                const double2* __restrict__ om) {
+  constexpr int N = C::N, n = C::n, m = C::m, B = C::B, Bh = C::Bh, NPAIR = C::NPAIR;
+  double2 z = make_double2(0.0, 0.0);
   if (tt > 0) {
     if (job < NPAIR + C::Bm) {
       const double2 w = __ldg(mkh + tt);
@@ -915,6 +1034,21 @@ __device__ __forceinline__ void inverse_fill(const double* T, double2* W, const 
     }
   }
   __syncthreads();
+}
+
+// Inverse transform of the slots in R (in place): fill + FFT, W = R.
+template <class C>
+__device__ __forceinline__ void inverse_fft_inplace(double* R, const double2* __restrict__ tw,
+                                                    const double2* __restrict__ mkh, const double2* __restrict__ om) {
+  using PL = Plan<C::N, few_plan<C>()>;
+  double2* W = reinterpret_cast<double2*>(R);
+  if constexpr (SFEM_MID_FUSED_FILL && !C::PAD) {
+    fft_pass_first<C, PL::R[0]>(W, tw, [&](int job, int t) { return inverse_elem<C>(R, job, t, mkh, om); });
+    fft<C, 1, PL::R[0]>(W, tw);
+  } else {
+    inverse_fill<C>(R, W, mkh, om);
+    fft<C>(W, tw);
+  }
 }
 
 // ------------------------------------------------------------ inverse post
@@ -1129,17 +1263,15 @@ __global__ void __launch_bounds__(TH, mid_min_blocks(TH))  // <= 128 registers
   SFEM_PT(1);
 
   if (MODE != kInverse) {
-    forward_fill<C>(R, R, PS, t.om);
-    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    forward_fft_inplace<C>(R, PS, t.tw, t.om);
     centre_reduce<C>(PS, C0);  // PS / C0 are outside the region
     forward_post<C>(reinterpret_cast<const double2*>(R), R, t.mk);
   }
   SFEM_PT(2);
-  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last, t.eigT);
   SFEM_PT(3);
   if (MODE != kForward) {
-    inverse_fill<C>(R, reinterpret_cast<double2*>(R), t.mkh, t.om);
-    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    inverse_fft_inplace<C>(R, t.tw, t.mkh, t.om);
     inverse_post<C>(reinterpret_cast<const double2*>(R), R, C0);
   }
   SFEM_PT(4);
@@ -1262,8 +1394,7 @@ __global__ void __launch_bounds__(TH, mid_min_blocks(TH))
   SFEM_PT(1);
   SymbolInfo nosym{};
   if (MODE != kInverse) {
-    forward_fill<C>(R, R, PS, t.om);
-    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    forward_fft_inplace<C>(R, PS, t.tw, t.om);
     centre_reduce<C>(PS, C0);
     forward_post<C>(reinterpret_cast<const double2*>(R), R, t.mk);
   }
@@ -1271,8 +1402,7 @@ __global__ void __launch_bounds__(TH, mid_min_blocks(TH))
   mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, nullptr, t.eig, nosym.f_last);
   SFEM_PT(3);
   if (MODE != kForward) {
-    inverse_fill<C>(R, reinterpret_cast<double2*>(R), t.mkh, t.om);
-    fft<C>(reinterpret_cast<double2*>(R), t.tw);
+    inverse_fft_inplace<C>(R, t.tw, t.mkh, t.om);
     inverse_post<C>(reinterpret_cast<const double2*>(R), R, C0);
   }
   SFEM_PT(4);
@@ -1393,7 +1523,7 @@ __global__ void __launch_bounds__(TH, 1)
     centre_reduce<C>(PS, C0);
     forward_post<C, true>(Zf, R, t.mk);
   }
-  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last);
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, base, t.eig, sym.f_last, t.eigT);
   if (MODE != kForward) {
 #if SFEM_MID_GW_DISCARD
     if (MODE == kForwardDivideInverse) {  // the forward result is dead (mix ended with a barrier)
