@@ -767,6 +767,14 @@ __device__ __forceinline__ void mix_zero(int b, const double* C0, double* CI, co
   }
 }
 
+// FFT tables (tw | mkh | om, N complex each) in constant memory
+// (SFEM_ROWS_CONST_TAB): the lookups leave the L1 / shared data pipe, which is
+// what bounds this kernel, for the constant cache.  They depend on N = 64 only.
+#ifndef SFEM_ROWS_CONST_TAB
+#define SFEM_ROWS_CONST_TAB 0
+#endif
+__constant__ double2 c_tab64[3 * N];
+
 template <int NN>
 __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB(NN))
     sweep_rows_fused(DevTable t, double* data, RowSegs segs, long long nrows, SymbolInfo sym,
@@ -778,9 +786,15 @@ __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB(NN))
   double* CI = smem + C::CI_OFF;
   double* base = smem + C::BASE_OFF;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + C::BAR_OFF);
+#if SFEM_ROWS_CONST_TAB
+  const double2* tw = c_tab64;
+  const double2* mkh = c_tab64 + N;
+  const double2* om = c_tab64 + 2 * N;
+#else
   double2* tw = reinterpret_cast<double2*>(smem + C::TAB_OFF);
   double2* mkh = tw + N;
   double2* om = mkh + N;
+#endif
   int* soff = reinterpret_cast<int*>(smem + C::SOFF_OFF);
   const int tid = threadIdx.x;
   const long long l0 = static_cast<long long>(blockIdx.x) * B;
@@ -825,11 +839,13 @@ __global__ void __launch_bounds__(Cfg<NN>::THREADS, SFEM_ROWS_MINB(NN))
       if (ii < sym.nlead) sacc += terms[ii];
     base[tid] = sacc;
   }
+#if !SFEM_ROWS_CONST_TAB
   for (int i = tid; i < N; i += C::THREADS) {
     tw[i] = t.tw[i];
     mkh[i] = t.mkh[i];
     om[i] = t.om[i];
   }
+#endif
 #if SFEM_ROWS_ROLLED_MIX
   if (tid < 2 * NN * 4) soff[tid] = srow<NN>((tid >> 2) % NN, 4 * (tid / (4 * NN)) + (tid & 3));
 #endif
@@ -882,6 +898,24 @@ cudaError_t launch_nn(const DevTable& t, double* data, const RowSegs& segs, long
   auto kern = sweep_rows_fused<NN>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (err != cudaSuccess) return err;
+#if SFEM_ROWS_CONST_TAB
+  {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      err = cudaMemcpyToSymbolAsync(c_tab64, t.tw, N * sizeof(double2), 0, cudaMemcpyDeviceToDevice, stream);
+      if (err == cudaSuccess)
+        err = cudaMemcpyToSymbolAsync(c_tab64, t.mkh, N * sizeof(double2), N * sizeof(double2),
+                                      cudaMemcpyDeviceToDevice, stream);
+      if (err == cudaSuccess)
+        err = cudaMemcpyToSymbolAsync(c_tab64, t.om, N * sizeof(double2), 2 * N * sizeof(double2),
+                                      cudaMemcpyDeviceToDevice, stream);
+      if (err != cudaSuccess) return err;
+      done[dev] = true;
+    }
+  }
+#endif
   const dim3 grid(static_cast<unsigned>((nrows + B - 1) / B));
   kern<<<grid, C::THREADS, C::SMEM, stream>>>(t, data, segs, nrows, sym, t.e0_fwd_w);
   return cudaGetLastError();
