@@ -174,6 +174,39 @@ def test_random_solves_match_oracle(sfem, orders, elements, lengths, shift):
     assert rel_l2(u, want) <= TOL
 
 
+@pytest.mark.parametrize("orders,elements", [
+    ([4, 2], [256, 2]),          # TMA strided tile wider than the last axis (3 dofs < 8 lines)
+    ([2, 4, 1], [3, 256, 4]),    # middle axis strided, ragged last-axis blocks (3 dofs)
+    ([9, 1, 2], [114, 5, 3]),    # K = 114 on axis 0 (5 boxes of 206 rows), 5 x 5 outer
+    ([1, 2, 2], [1024, 3, 5]),   # n = 1 four-line tiles, 9 last-axis dofs = 2 full tiles + 1 line
+    ([2, 2, 1, 4], [2, 512, 3, 2]),   # 4-D: K = 512 strided with two outer axes
+    ([9, 2], [1024, 4]),         # C3's two-line tiles, 7 last-axis dofs (odd)
+])
+def test_mid_tma_tiles_ragged_shapes(sfem, orders, elements, monkeypatch):
+    # strided sweeps with TMA tiles (sweep_mid_tma): partial tiles rely on the
+    # TMA unit's zero fill / clipping; same solve with the cp.async kernels
+    N = len(orders)
+    spec = sfem.ProblemSpec(N, [1.0] * N, elements, orders, 0.5)
+    f = np.random.default_rng(sum(elements)).uniform(-1, 1, spec.extents())
+    u, _ = sfem.solve_dof(spec, f)
+    want = O.solve_full_diagonalization(f, orders, elements, [1.0] * N, 0.5)
+    assert rel_l2(u, want) <= TOL
+    # a tensor with a caller pitch (device entry): pad columns must stay untouched
+    import torch
+    plan = sfem.Plan(spec)
+    ext = plan.extents
+    pitch = plan.pitch + 4
+    rows = plan.unknowns // ext[-1]
+    d = torch.full((rows, pitch), 7.0, dtype=torch.float64, device="cuda")
+    d[:, :ext[-1]] = torch.from_numpy(f.reshape(rows, ext[-1]))
+    torch.cuda.synchronize()
+    plan.solve_device(d.data_ptr(), pitch=pitch)
+    torch.cuda.synchronize()
+    got = d.cpu().numpy()
+    assert rel_l2(got[:, :ext[-1]].reshape(ext), want) <= TOL
+    assert np.all(got[:, ext[-1] + 1:] == 7.0)   # (the first pad element may be written by even-length row copies)
+
+
 def test_device_solve_is_deterministic(sfem):
     # test_poisson.cpp:355-362 (bitwise independence of the thread count) -> run to run
     spec = sfem.ProblemSpec(3, [1.0] * 3, [8] * 3, [9] * 3, 0.0)
