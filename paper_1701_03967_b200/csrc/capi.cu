@@ -399,7 +399,8 @@ Step strided_step(const View& v, int a, int mode) {
     }
     s.geo.nbox = static_cast<int>((v.ext[a] + 255) / 256);
     s.geo.boxp = static_cast<int>((v.ext[a] + s.geo.nbox - 1) / s.geo.nbox);
-    const int balign = std::max(1, 16 / tb);  // boxes start 128-byte aligned in shared memory
+    // boxes start 128-byte aligned in shared memory: boxp * tb a multiple of 16 doubles
+    const int balign = tb % 16 == 0 ? 1 : (tb % 8 == 0 ? 2 : (tb % 4 == 0 ? 4 : (tb % 2 == 0 ? 8 : 16)));
     s.geo.boxp = (s.geo.boxp + balign - 1) / balign * balign;
     s.geo.nblk0 = (v.ext[N - 1] + tb - 1) / tb;
     s.geo.ext0 = v.ext[N - 1];

@@ -1340,7 +1340,7 @@ struct TmaShape {
   using C = Cfg<NN, K, BB, TH, false>;
   static constexpr int NBOX = (C::L + 255) / 256;
   // every box starts 128-byte aligned in shared memory: BOXP * BB a multiple of 16 doubles
-  static constexpr int BALIGN = 16 / BB > 0 ? 16 / BB : 1;
+  static constexpr int BALIGN = BB % 16 == 0 ? 1 : (BB % 8 == 0 ? 2 : (BB % 4 == 0 ? 4 : (BB % 2 == 0 ? 8 : 16)));
   static constexpr int BOXP = ((C::L + NBOX - 1) / NBOX + BALIGN - 1) / BALIGN * BALIGN;
   // the boxes' zero-filled tail rows must fit the region; 16-byte box rows at least
   static constexpr bool OK = NBOX * BOXP * BB <= C::REGION && (BB * 8) % 16 == 0;
