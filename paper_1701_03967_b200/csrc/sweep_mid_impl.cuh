@@ -391,12 +391,51 @@ __host__ __device__ constexpr bool few_plan() {
                            : (C::J <= 8 || C::THREADS >= SFEM_MID_FEW_TH);
 }
 
+// One thread group per job (C2's packed one-line tiles: J = 3 jobs x 256
+// radix-16 butterflies = 768 threads): the passes of a job only depend on that
+// job's data, so each group of N/R threads runs its job's passes behind its
+// own named barrier and the three groups drift apart -- one group's
+// shared-memory phase overlaps another's butterflies (with block barriers all
+// 24 warps sat in the same phase of every pass).
+#ifndef SFEM_MID_GROUPED_FFT
+#define SFEM_MID_GROUPED_FFT 0  // measured slower on C2 (1.01 -> 1.28 ms: the job-major thread map makes the first pass's stores 8-way conflicted)
+#endif
+template <class C, int R>
+__host__ __device__ constexpr bool grouped_fft() {
+  return SFEM_MID_GROUPED_FFT && C::PK && C::THREADS == C::J * (C::N / R) && (C::N / R) % 32 == 0 && C::J <= 15;
+}
+
+template <class C, int R, int NS>
+__device__ __forceinline__ void fft_pass_grouped(double2* W, const double2* __restrict__ tw) {
+  constexpr int N = C::N, J = C::J, NR = N / R;
+  constexpr int TSTEP = N / (NS * R);
+  const int job = threadIdx.x / NR, j = threadIdx.x - job * NR, k = j % NS;
+  double2 v[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    double2 a = W[(j + q * NR) * J + job];
+    if (NS > 1 && q > 0) a = c_mul(a, __ldg(tw + (q * k * TSTEP) % N));
+    v[q] = a;
+  }
+  dft<R, N>(v, tw);
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + job), "r"(NR) : "memory");
+  const int outb = (j / NS) * NS * R + k;
+#pragma unroll
+  for (int pp = 0; pp < R; ++pp) W[(outb + pp * NS) * J + job] = v[pp];
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + job), "r"(NR) : "memory");
+}
+
 template <class C, int P = 0, int NS = 1>
 __device__ __forceinline__ void fft(double2* W, const double2* __restrict__ tw) {
   using PL = Plan<C::N, few_plan<C>()>;
   if constexpr (P < PL::NP && SFEM_MID_DIAG_SKIP != 1) {
     constexpr int R = PL::R[P];
-    fft_pass<C, R, NS>(W, tw);
+    if constexpr (grouped_fft<C, R>()) {
+      fft_pass_grouped<C, R, NS>(W, tw);
+      if constexpr (P + 1 == PL::NP) __syncthreads();  // the post stage reads every job
+    } else {
+      fft_pass<C, R, NS>(W, tw);
+    }
     fft<C, P + 1, NS * R>(W, tw);
   }
 }
