@@ -363,27 +363,46 @@ __device__ __forceinline__ void forward_job(const Job& jb, const double* T, doub
       sA = sB;
       sB = t_;
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = h == 0 ? jb.q1 : jb.q2;
-      Unroll<G>::run([&](auto PP) {
-        constexpr int p = decltype(PP)::value;
-        if (p == 0 && q == 0) return;  // k = 0
-        const int k = q + R * p;
-        const double2 zk = h == 0 ? w1[p] : w2[p];
-        const double2 zc = partner<p>(w1, w2, jb.tau, h, false);
-        // r1 = Re(mk_k V1), r2 = Re(mk_k V2), V1 = (Z_k + conj Z_{N-k})/2,
-        // V2 = (Z_k - conj Z_{N-k})/(2i); the 1/2 is folded into mkh
-        const double2 w = mkh[k];
-        const double r1 = fma(w.x, zk.x + zc.x, w.y * (zk.y - zc.y));
-        const double r2 = fma(w.x, zk.y + zc.y, -w.y * (zk.x - zc.x));
+    // r1 = Re(mk_k V1), r2 = Re(mk_k V2), V1 = (Z_k + conj Z_{N-k})/2,
+    // V2 = (Z_k - conj Z_{N-k})/(2i); the 1/2 is folded into mkh.  One pass over
+    // the (k, N-k) pairs: both outputs share the four sums / differences and a
+    // pair's values are dead once emitted (sweep_fast.cu forward_post):
+    //   tau != 0: (w1[p], w2[7-p]); tau == 0: class 0 pairs with itself
+    //   (w1[p], w1[8-p]) p = 1..3, k = 32 alone; class 4 (w2[p], w2[7-p]) p = 0..3
+    auto emit_pair = [&](int k, const double2 zk, const double2 zc, bool both) {
+      const double sx = zk.x + zc.x, dy = zk.y - zc.y, sy = zk.y + zc.y, dx = zk.x - zc.x;
+      const double2 w = mkh[k];
+      const double r1 = fma(w.x, sx, w.y * dy), r2 = fma(w.x, sy, -w.y * dx);
+      if (jb.kind == 0) {
+        sA[k] = r1;
+        sB[N - k] = r2;
+      } else {
+        sA[N - k] = r1;
+        sB[N - k] = r2;
+      }
+      if (both) {
+        const double2 u = mkh[N - k];
+        const double t1 = fma(u.x, sx, -u.y * dy), t2 = fma(u.x, sy, u.y * dx);
         if (jb.kind == 0) {
-          sA[k] = r1;
-          sB[N - k] = r2;
+          sA[N - k] = t1;
+          sB[k] = t2;
         } else {
-          sA[N - k] = r1;
-          sB[N - k] = r2;
+          sA[k] = t1;
+          sB[k] = t2;
         }
+      }
+    };
+    const bool t0 = jb.tau == 0;
+    Unroll<G>::run([&](auto PP) {
+      constexpr int p = decltype(PP)::value;
+      const double2 y = t0 ? w1[(G - p) % G] : w2[G - 1 - p];
+      const bool active = !t0 || (p >= 1 && p <= G / 2);
+      if (active) emit_pair(jb.q1 + R * p, w1[p], y, !t0 || p < G / 2);
+    });
+    if (t0) {
+      Unroll<G / 2>::run([&](auto PP) {
+        constexpr int p = decltype(PP)::value;
+        emit_pair(jb.q2 + R * p, w2[p], w2[G - 1 - p], true);
       });
     }
   } else {
