@@ -54,6 +54,48 @@ extern template cudaError_t launch_auto_n<768>(const DevTable&, const LineSet&, 
                                                   cudaStream_t);
 extern template cudaError_t launch_auto_n<1000>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
                                                   cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<16>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<24>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<32>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<40>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<48>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<64>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<80>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<96>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<100>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<128>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<160>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<192>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<200>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<256>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<320>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<384>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<512>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<768>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<1000>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<1024>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
+extern template cudaError_t launch_auto_tma_n<2048>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                     cudaStream_t);
 }  // namespace mid
 
 // Lines per tile and threads per CTA of the C5 shapes.
@@ -135,6 +177,8 @@ static bool mid_tma_enabled() {
   return v;
 }
 
+bool mid_auto(int n, int K);
+
 int mid_tma_lines(int n, int K) {
   if (!mid_tma_enabled()) return 0;
   if (n == 1 && K == 1024) return SFEM_MID_B_N1;
@@ -142,7 +186,35 @@ int mid_tma_lines(int n, int K) {
   if (n == 4 && K == 256) return SFEM_MID_B_N4;
   if (n == 9 && K == 114) return SFEM_MID_B_N9;
   if (n == 9 && K == 1024) return 2;
+#if SFEM_MID_AUTO
+  if (!mid_auto(n, K)) return 0;
+  switch (K) {
+    case 16: return mid::auto_tma_lines_n<16>(n);
+    case 24: return mid::auto_tma_lines_n<24>(n);
+    case 32: return mid::auto_tma_lines_n<32>(n);
+    case 40: return mid::auto_tma_lines_n<40>(n);
+    case 48: return mid::auto_tma_lines_n<48>(n);
+    case 64: return mid::auto_tma_lines_n<64>(n);
+    case 80: return mid::auto_tma_lines_n<80>(n);
+    case 96: return mid::auto_tma_lines_n<96>(n);
+    case 100: return mid::auto_tma_lines_n<100>(n);
+    case 128: return mid::auto_tma_lines_n<128>(n);
+    case 160: return mid::auto_tma_lines_n<160>(n);
+    case 192: return mid::auto_tma_lines_n<192>(n);
+    case 200: return mid::auto_tma_lines_n<200>(n);
+    case 256: return mid::auto_tma_lines_n<256>(n);
+    case 320: return mid::auto_tma_lines_n<320>(n);
+    case 384: return mid::auto_tma_lines_n<384>(n);
+    case 512: return mid::auto_tma_lines_n<512>(n);
+    case 768: return mid::auto_tma_lines_n<768>(n);
+    case 1000: return mid::auto_tma_lines_n<1000>(n);
+    case 1024: return mid::auto_tma_lines_n<1024>(n);
+    case 2048: return mid::auto_tma_lines_n<2048>(n);
+    default: return 0;
+  }
+#else
   return 0;
+#endif
 }
 
 cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
@@ -157,6 +229,32 @@ cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaG
   if (t.n == 9 && t.K == 114)
     return mid::launch_tma<9, 114, SFEM_MID_B_N9, SFEM_MID_TH_N9>(t, tmap, geo, mode, analysis, stream);
   if (t.n == 9 && t.K == 1024) return mid::launch_tma<9, 1024, 2, SFEM_MID_C3_TH>(t, tmap, geo, mode, analysis, stream);
+#if SFEM_MID_AUTO
+  switch (t.K) {
+    case 16: return mid::launch_auto_tma_n<16>(t, tmap, geo, mode, analysis, stream);
+    case 24: return mid::launch_auto_tma_n<24>(t, tmap, geo, mode, analysis, stream);
+    case 32: return mid::launch_auto_tma_n<32>(t, tmap, geo, mode, analysis, stream);
+    case 40: return mid::launch_auto_tma_n<40>(t, tmap, geo, mode, analysis, stream);
+    case 48: return mid::launch_auto_tma_n<48>(t, tmap, geo, mode, analysis, stream);
+    case 64: return mid::launch_auto_tma_n<64>(t, tmap, geo, mode, analysis, stream);
+    case 80: return mid::launch_auto_tma_n<80>(t, tmap, geo, mode, analysis, stream);
+    case 96: return mid::launch_auto_tma_n<96>(t, tmap, geo, mode, analysis, stream);
+    case 100: return mid::launch_auto_tma_n<100>(t, tmap, geo, mode, analysis, stream);
+    case 128: return mid::launch_auto_tma_n<128>(t, tmap, geo, mode, analysis, stream);
+    case 160: return mid::launch_auto_tma_n<160>(t, tmap, geo, mode, analysis, stream);
+    case 192: return mid::launch_auto_tma_n<192>(t, tmap, geo, mode, analysis, stream);
+    case 200: return mid::launch_auto_tma_n<200>(t, tmap, geo, mode, analysis, stream);
+    case 256: return mid::launch_auto_tma_n<256>(t, tmap, geo, mode, analysis, stream);
+    case 320: return mid::launch_auto_tma_n<320>(t, tmap, geo, mode, analysis, stream);
+    case 384: return mid::launch_auto_tma_n<384>(t, tmap, geo, mode, analysis, stream);
+    case 512: return mid::launch_auto_tma_n<512>(t, tmap, geo, mode, analysis, stream);
+    case 768: return mid::launch_auto_tma_n<768>(t, tmap, geo, mode, analysis, stream);
+    case 1000: return mid::launch_auto_tma_n<1000>(t, tmap, geo, mode, analysis, stream);
+    case 1024: return mid::launch_auto_tma_n<1024>(t, tmap, geo, mode, analysis, stream);
+    case 2048: return mid::launch_auto_tma_n<2048>(t, tmap, geo, mode, analysis, stream);
+    default: break;
+  }
+#endif
   return cudaErrorNotSupported;
 }
 

@@ -1710,6 +1710,62 @@ cudaError_t launch_auto_n(const DevTable& t, const LineSet& ls, int mode, int an
   }
 }
 
+// General shapes, strided sweeps with TMA tiles (sweep_mid_tma): the same
+// tile shape as launch_auto; lines per tile 0 when the shape has no TMA kernel.
+template <int NN, int K>
+constexpr int auto_tma_lines() {
+  using S = AutoShape<NN, K>;
+  if constexpr (S::B < 2 || served_elsewhere<NN, K>()) {
+    return 0;
+  } else {
+    return TmaShape<NN, K, S::B, S::TH>::OK ? S::B : 0;
+  }
+}
+
+template <int NN, int K>
+cudaError_t launch_auto_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
+                            cudaStream_t stream) {
+  if constexpr (auto_tma_lines<NN, K>() == 0) {
+    return cudaErrorNotSupported;
+  } else {
+    using S = AutoShape<NN, K>;
+    return launch_tma<NN, K, S::B, S::TH>(t, tmap, geo, mode, analysis, stream);
+  }
+}
+
+template <int K>
+cudaError_t launch_auto_tma_n(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
+                              cudaStream_t stream) {
+  switch (t.n) {
+    case 1: return launch_auto_tma<1, K>(t, tmap, geo, mode, analysis, stream);
+    case 2: return launch_auto_tma<2, K>(t, tmap, geo, mode, analysis, stream);
+    case 3: return launch_auto_tma<3, K>(t, tmap, geo, mode, analysis, stream);
+    case 4: return launch_auto_tma<4, K>(t, tmap, geo, mode, analysis, stream);
+    case 5: return launch_auto_tma<5, K>(t, tmap, geo, mode, analysis, stream);
+    case 6: return launch_auto_tma<6, K>(t, tmap, geo, mode, analysis, stream);
+    case 7: return launch_auto_tma<7, K>(t, tmap, geo, mode, analysis, stream);
+    case 8: return launch_auto_tma<8, K>(t, tmap, geo, mode, analysis, stream);
+    case 9: return launch_auto_tma<9, K>(t, tmap, geo, mode, analysis, stream);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+template <int K>
+int auto_tma_lines_n(int n) {
+  switch (n) {
+    case 1: return auto_tma_lines<1, K>();
+    case 2: return auto_tma_lines<2, K>();
+    case 3: return auto_tma_lines<3, K>();
+    case 4: return auto_tma_lines<4, K>();
+    case 5: return auto_tma_lines<5, K>();
+    case 6: return auto_tma_lines<6, K>();
+    case 7: return auto_tma_lines<7, K>();
+    case 8: return auto_tma_lines<8, K>();
+    case 9: return auto_tma_lines<9, K>();
+    default: return 0;
+  }
+}
+
 template <int K>
 bool auto_ok_n(int n) {
   switch (n) {
