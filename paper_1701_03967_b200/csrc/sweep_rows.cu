@@ -381,7 +381,8 @@ __device__ __forceinline__ void forward_job(const Job& jb, const double* T, doub
         sB[N - k] = r2;
       }
       if (both) {
-        const double2 u = mkh[N - k];
+        // mkh[N-k] = 0.5 exp(i pi/2 - i pi k/2N) = (w.y, w.x): no second table load
+        const double2 u = make_double2(w.y, w.x);
         const double t1 = fma(u.x, sx, -u.y * dy), t2 = fma(u.x, sy, u.y * dx);
         if (jb.kind == 0) {
           sA[N - k] = t1;
