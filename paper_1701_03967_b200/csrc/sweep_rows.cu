@@ -458,6 +458,54 @@ __device__ __forceinline__ void inverse_job(const Job& jb, double* T, double* X,
     // slot of line b); imaginary part: DCT-III of b~ (reversed even slot)
     const double* A = X + sbase(jb.j) + (jb.kind == 0 ? SR : 0);
     const double* Bs = X + sbase(jb.j) + (jb.kind == 0 ? 0 : SR);
+#if SFEM_ROWS_INV_PAIRS
+    // One evaluation per (t, N-t) pair: the pair shares its four slot values,
+    // the table entry (mkh[N-t] is mkh[t] with its components swapped) and
+    // the two products -- V1' = conj(V1), V2' = conj(V2), so z_t = conj(V1 + i V2)
+    // and z_{N-t} = V1 - i V2.  Half the slot and table loads and half the
+    // products of the per-element form.  tau != 0: t = c1 + 8p pairs with class
+    // c2 at index 7-p; tau == 0: class 0 pairs with itself (t = 8p, p = 1..3;
+    // t = 32 alone; t = 0 unused) and so does class 4 (t = 4 + 8r, r = 0..3).
+    const bool t0 = jb.tau == 0;
+    double2 za[R], zb[R];
+    Unroll<R>::run([&](auto P_) {
+      constexpr int p = decltype(P_)::value;
+      constexpr int T0[8] = {4, 8, 16, 24, 32, 12, 20, 28};
+      const int t = t0 ? T0[p] : jb.tau + G * p;
+      const double2 w = mkh[t];
+      double ax, ar;
+      if (jb.kind == 0) {
+        ax = A[t];
+        ar = A[N - t];
+      } else {
+        ax = A[N - t];
+        ar = A[t];
+      }
+      const double bx = Bs[N - t], br = Bs[t];
+      // V1 = w (ax - i ar), V2 = w (bx - i br)
+      const double v1x = fma(w.x, ax, w.y * ar), v1y = fma(w.y, ax, -w.x * ar);
+      const double v2x = fma(w.x, bx, w.y * br), v2y = fma(w.y, bx, -w.x * br);
+      za[p] = make_double2(v1x - v2y, -(v1y + v2x));
+      zb[p] = make_double2(v1x + v2y, v1y - v2x);
+    });
+    const double2 zero = make_double2(0.0, 0.0);
+    v[0][0] = t0 ? zero : za[0];
+    v[0][1] = za[1];
+    v[0][2] = za[2];
+    v[0][3] = za[3];
+    v[0][4] = za[4];
+    v[0][5] = t0 ? zb[3] : za[5];
+    v[0][6] = t0 ? zb[2] : za[6];
+    v[0][7] = t0 ? zb[1] : za[7];
+    v[1][0] = t0 ? za[0] : zb[7];
+    v[1][1] = t0 ? za[5] : zb[6];
+    v[1][2] = t0 ? za[6] : zb[5];
+    v[1][3] = t0 ? za[7] : zb[4];
+    v[1][4] = t0 ? zb[7] : zb[3];
+    v[1][5] = t0 ? zb[6] : zb[2];
+    v[1][6] = t0 ? zb[5] : zb[1];
+    v[1][7] = zb[0];
+#else
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = h == 0 ? jb.c1 : jb.c2;
@@ -484,6 +532,7 @@ __device__ __forceinline__ void inverse_job(const Job& jb, double* T, double* X,
         v[h][r] = z;
       }
     }
+#endif
   }
   __syncwarp();  // the warp's S rows are read: exchange data overwrites them
   if (jb.kind < 3) {
@@ -606,6 +655,9 @@ __host__ __device__ constexpr int srow_c(int s, int b) {
 // tile and warp; with three CTAs in different phases the fused kernel's 93 KB
 // of code did not stay in the instruction caches (ncu: no_instruction was the
 // top stall reason, 1.2-2.7 per issue).
+#ifndef SFEM_ROWS_INV_PAIRS
+#define SFEM_ROWS_INV_PAIRS 1
+#endif
 #ifndef SFEM_ROWS_ROLLED_MIX
 #define SFEM_ROWS_ROLLED_MIX 1
 #endif

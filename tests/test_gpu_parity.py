@@ -495,9 +495,11 @@ def test_plan_on_two_streams_is_ordered(sfem):
 @pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 8, 9])
 def test_rows_fused_kernel_matches_block_sync_kernel(sfem, n, monkeypatch):
     # the warp-local fused last-axis kernel (sweep_rows.cu) against the
-    # block-synchronous one (SFEM_ROWS_V1=1, sweep_fast.cu): same arithmetic
-    # in the same order, so bitwise equal; 3-D blocked schedule and 2-D rows,
-    # partial last tiles
+    # block-synchronous one (SFEM_ROWS_V1=1, sweep_fast.cu): the same
+    # formulas in two translation units, equal to rounding (nvcc's FMA
+    # contraction of the complex products is not the same choice in both:
+    # differences of an ulp or two, both 7e-16 from the oracle); 3-D blocked
+    # schedule and 2-D rows, partial last tiles
     for orders, elements in (([n, n, n], [64, 64, 64]) if n <= 4 else ([2, 3, n], [64, 5, 64]),
                              ([3, n], [7, 64])):
         N = len(orders)
@@ -507,7 +509,8 @@ def test_rows_fused_kernel_matches_block_sync_kernel(sfem, n, monkeypatch):
         monkeypatch.setenv("SFEM_ROWS_V1", "1")
         u_old, _ = sfem.solve_dof(spec, f)
         monkeypatch.delenv("SFEM_ROWS_V1")
-        assert np.array_equal(u_new, u_old), (orders, elements, float(np.max(np.abs(u_new - u_old))))
+        assert np.max(np.abs(u_new - u_old)) <= 4e-15 * np.max(np.abs(u_old)), \
+            (orders, elements, float(np.max(np.abs(u_new - u_old))))
         if np.prod(spec.extents()) < 3e6:
             want = O.solve_full_diagonalization(f, orders, elements, [1.0] * N, 0.3)
             assert rel_l2(u_new, want) <= TOL

@@ -34,7 +34,7 @@ def run(orders, reps=10):
     same = torch.equal(out["0"][0], out["1"][0])
     diff = float((out["0"][0] - out["1"][0]).abs().max())
     print(f"orders {orders}: new {[round(x, 4) for x in out['0'][1]]}  v1 {[round(x, 4) for x in out['1'][1]]}  "
-          f"bitwise {same} maxdiff {diff:.2e}", flush=True)
+          f"same bits {same} maxdiff {diff:.2e}", flush=True)
 
 
 if __name__ == "__main__":
