@@ -655,6 +655,9 @@ __host__ __device__ constexpr int srow_c(int s, int b) {
 // tile and warp; with three CTAs in different phases the fused kernel's 93 KB
 // of code did not stay in the instruction caches (ncu: no_instruction was the
 // top stall reason, 1.2-2.7 per issue).
+#ifndef SFEM_ROWS_MIX_PREFETCH
+#define SFEM_ROWS_MIX_PREFETCH 0
+#endif
 #ifndef SFEM_ROWS_INV_PAIRS
 #define SFEM_ROWS_INV_PAIRS 1
 #endif
@@ -692,16 +695,35 @@ __device__ __forceinline__ void mix_item_rolled(int item, double* X, const doubl
 #pragma unroll
   for (int bb = 0; bb < 4; ++bb) bs[bb] = base[4 * g + bb];
   const double* mk = mixT + k;
+#if SFEM_ROWS_MIX_PREFETCH
+  // software pipeline: column l+1's matrix entries are loaded before column
+  // l's divides (their dependent chains then hide the L1 latency)
+  double mvn[NN];
+#pragma unroll
+  for (int s = 0; s < NN; ++s) mvn[s] = __ldg(mk + s * NN * N);
+#endif
 #pragma unroll 1
   for (int l = 0; l < NN; ++l) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     const double* ml = mk + l * N;
+#if SFEM_ROWS_MIX_PREFETCH
+#pragma unroll
+    for (int s = 0; s < NN; ++s) {
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) acc[bb] = fma(mvn[s], vv[s][bb], acc[bb]);
+    }
+    if (l + 1 < NN) {
+#pragma unroll
+      for (int s = 0; s < NN; ++s) mvn[s] = __ldg(ml + N + s * NN * N);
+    }
+#else
 #pragma unroll
     for (int s = 0; s < NN; ++s) {
       const double mv = __ldg(ml + s * NN * N);
 #pragma unroll
       for (int bb = 0; bb < 4; ++bb) acc[bb] = fma(mv, vv[s][bb], acc[bb]);
     }
+#endif
     const double lam = f_last * __ldg(eig + l * N + k), ns = __ldg(nsq + l * N + k);
     const int4 o = so[l];
     Xk[o.x] = sym_div(acc[0], (bs[0] + lam) * ns);
