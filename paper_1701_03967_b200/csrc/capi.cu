@@ -327,6 +327,14 @@ struct View {
   }
 };
 
+bool mid_tma_prefetch() {
+  static const bool v = [] {
+    const char* e = std::getenv("SFEM_MID_PREFETCH");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // Sweep along strided axis a (a < N-1) of view v.
 Step strided_step(const View& v, int a, int mode) {
   const int N = v.N;
@@ -409,6 +417,8 @@ Step strided_step(const View& v, int a, int mode) {
     s.box[0] = static_cast<cuuint32_t>(tb);
     s.box[1] = static_cast<cuuint32_t>(s.geo.boxp);
     s.box[2] = s.box[3] = 1;
+    // L2 prefetch one resident wave ahead where the tile's rows are close (<= 16 KB apart)
+    s.geo.prefetch = (st[a] * 8 <= 16384 && mid_tma_prefetch()) ? 2 * 148 : 0;
   }
   return s;
 }

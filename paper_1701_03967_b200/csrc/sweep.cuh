@@ -87,6 +87,7 @@ struct TmaGeom {
   long long ext2;      // extent of d2
   long long ntiles;    // nblk0 * ext2 * ext3
   int ld_mode, st_mode, xblk;
+  int prefetch;        // mid kernels: L2-prefetch the tile this many tiles ahead (0 = off)
 };
 
 // Strided sweep through TMA (sweep_fast.cu).  `tmap` / `smap` are CUtensorMaps

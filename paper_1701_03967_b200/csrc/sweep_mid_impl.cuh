@@ -1426,6 +1426,24 @@ __global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))
           "[%6];\n" ::"r"(mid_smem_u32(R + j * TS::BOXP * BB)),
           "l"(&tmap), "r"(c0), "r"(j * TS::BOXP), "r"(c2), "r"(c3), "r"(mid_smem_u32(bar))
           : "memory");
+    if (geo.prefetch > 0) {
+      // L2 prefetch of the tile the next CTA on this SM will load (one resident
+      // wave ahead).  Only for sweeps whose positions are a few KB apart: C5
+      // n=4 axis-1 sweeps -6 %, but +22 % along axis 0, whose rows are planes
+      // apart (profiles/r3z4_mid_tma_prefetch.txt), so the host turns it on per sweep.
+      const long long lin = (static_cast<long long>(c3) * geo.ext2 + c2) * geo.nblk0 + c0 / BB;
+      const long long nxt = lin + geo.prefetch;
+      if (nxt < geo.ntiles) {
+        const int p0 = static_cast<int>(nxt % geo.nblk0) * BB;
+        const long long rest = nxt / geo.nblk0;
+        const int p2 = static_cast<int>(rest % geo.ext2), p3 = static_cast<int>(rest / geo.ext2);
+#pragma unroll 1
+        for (int j = 0; j < TS::NBOX; ++j)
+          asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];\n" ::"l"(&tmap), "r"(p0),
+                       "r"(j * TS::BOXP), "r"(p2), "r"(p3)
+                       : "memory");
+      }
+    }
   }
   __syncthreads();  // the barrier is initialised before anyone polls it
   asm volatile(
