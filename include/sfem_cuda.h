@@ -282,6 +282,12 @@ int sfem_cuda_dist_solve_stats(sfem_dist dist, double* phase_ms, long long* byte
  * copies (the single-GPU check of the chunked schedule: same phases, chunks and
  * message lists as sfem_cuda_dist_solve). */
 int sfem_cuda_dist_setup(sfem_dist dist, int chunks);
+/* The messages of exchange `step` (1 or 2), chunk `chunk`, of this rank, in
+ * issue order: n_send sends then n_recv receives, each (peer, offset, count) in
+ * doubles (offsets into the send / receive exchange buffer).  peers / offsets /
+ * counts (capacity entries each) may be NULL to query the counts. */
+int sfem_cuda_dist_messages(sfem_dist dist, int step, int chunk, int capacity, int* n_send, int* n_recv, int* peers,
+                            long long* offsets, long long* counts);
 int sfem_cuda_dist_solve_group(sfem_dist* dists, int n, double* const* d_xs, void* stream);
 
 /* ---- Multi-GPU with the exchanges fused into the sweeps over NVLink ----

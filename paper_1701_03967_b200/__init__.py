@@ -135,6 +135,8 @@ _SIGS = [
     ("sfem_cuda_dist_solve", ctypes.c_int, [_vp, _vp, _vp]),
     ("sfem_cuda_dist_solve_stats", ctypes.c_int, [_vp, _dp, _llp]),
     ("sfem_cuda_dist_setup", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("sfem_cuda_dist_messages", ctypes.c_int,
+     [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip, _ip, _llp, _llp]),
     ("sfem_cuda_dist_solve_group", ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, ctypes.POINTER(_vp), _vp]),
 ]
 HEADER_SYMBOLS = [s[0] for s in _SIGS]

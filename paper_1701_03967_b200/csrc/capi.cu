@@ -2316,6 +2316,33 @@ int sfem_cuda_dist_setup(sfem_dist d, int chunks) {
   });
 }
 
+int sfem_cuda_dist_messages(sfem_dist d, int step, int chunk, int capacity, int* n_send, int* n_recv, int* peers,
+                            long long* offsets, long long* counts) {
+  return guarded([&] {
+    require(d && n_send && n_recv, "dist_messages: null argument");
+    require(d->C > 0, "dist_messages: plan not set up (sfem_cuda_dist_setup / dist_comm_init)");
+    require((step == 1 || step == 2) && chunk >= 0 && chunk < d->C, "dist_messages: bad step / chunk");
+    std::vector<Msg> sends, recvs;
+    if (step == 1)
+      msgs1(d, d->rank, chunk, sends, recvs);
+    else
+      msgs2(d, d->rank, chunk, sends, recvs);
+    *n_send = static_cast<int>(sends.size());
+    *n_recv = static_cast<int>(recvs.size());
+    require(static_cast<int>(sends.size() + recvs.size()) <= capacity || !peers,
+            "dist_messages: capacity too small");
+    if (!peers || !offsets || !counts) return;
+    int i = 0;
+    for (const auto* list : {&sends, &recvs})
+      for (const Msg& m : *list) {
+        peers[i] = m.peer;
+        offsets[i] = m.off;
+        counts[i] = m.count;
+        ++i;
+      }
+  });
+}
+
 int sfem_cuda_dist_comm_init(sfem_dist d, const void* id, int chunks) {
   return guarded([&] {
     require(d && id, "dist_comm_init: null argument");

@@ -56,6 +56,56 @@ def padded(lx: int) -> int:
     return lx + (lx & 1)
 
 
+def chunk_schedule(extents, nranks: int, chunks: int):
+    """Chunk rows of the library-owned exchange (capi.cu dist_setup): per rank
+    the x-row chunks (even starts, `partition_even` of its slab) and the y-row
+    chunks (`partition` of its y range).  Returns (xc0, xw, yc0, yw), each
+    [rank][chunk]."""
+    _, lxs = partition_even(extents[0], nranks)
+    _, lys = partition(extents[1], nranks)
+    xc0, xw, yc0, yw = [], [], [], []
+    for p in range(nranks):
+        o, w = partition_even(lxs[p], chunks)
+        xc0.append(o), xw.append(w)
+        o, w = partition(lys[p], chunks)
+        yc0.append(o), yw.append(w)
+    return xc0, xw, yc0, yw
+
+
+def chunk_messages(extents, nranks: int, rank: int, chunks: int, step: int, chunk: int):
+    """Messages of one exchange chunk as sfem_cuda_dist_solve issues them
+    (capi.cu msgs1 / msgs2): (sends, recvs), each a list of (peer, offset,
+    count) in doubles -- offsets into the rank's send buffer (A in exchange 1,
+    B in exchange 2) and receive buffer (B / A).  Messages between a pair of
+    ranks appear in the same order on both sides."""
+    x0s, lxs = partition_even(extents[0], nranks)
+    y0s, lys = partition(extents[1], nranks)
+    R = int(np.prod(extents[2:])) if len(extents) > 2 else 1
+    Q = extents[1] * R
+    xc0, xw, yc0, yw = chunk_schedule(extents, nranks, chunks)
+    r, c = rank, chunk
+    sends, recvs = [], []
+    if step == 1:
+        w = xw[r][c]
+        for p in range(nranks):
+            if w > 0 and lys[p] > 0:
+                sends.append((p, Q * xc0[r][c] + y0s[p] * R * padded(w), lys[p] * R * padded(w)))
+            ws = xw[p][c]
+            if ws > 0 and lys[r] > 0:
+                recvs.append((p, lys[r] * R * (x0s[p] + xc0[p][c]), lys[r] * R * padded(ws)))
+    else:
+        lyR = lys[r] * R
+        for p in range(nranks):
+            for cx in range(chunks):
+                wpp = padded(xw[p][cx])
+                if xw[p][cx] > 0 and yw[r][c] > 0:
+                    sends.append((p, lyR * (x0s[p] + xc0[p][cx]) + yc0[r][c] * R * wpp, yw[r][c] * R * wpp))
+                wpr = padded(xw[r][cx])
+                if xw[r][cx] > 0 and yw[p][c] > 0:
+                    recvs.append((p, Q * xc0[r][cx] + (y0s[p] + yc0[p][c]) * R * wpr, yw[p][c] * R * wpr))
+    return sends, recvs
+
+
 @dataclass
 class SlabShape:
     extents: List[int]
@@ -119,6 +169,19 @@ class DistPlan:
         """Chunk schedule and plan-owned buffers without a communicator
         (for solve_group)."""
         _check(lib.sfem_cuda_dist_setup(self.handle, chunks))
+
+    def messages(self, step: int, chunk: int):
+        """(sends, recvs) of one exchange chunk as the library issues them
+        (sfem_cuda_dist_messages): lists of (peer, offset, count)."""
+        cap = 4 * self.nranks * 16 + 16
+        ns, nr = ctypes.c_int(), ctypes.c_int()
+        peers = (ctypes.c_int * cap)()
+        offs = (ctypes.c_longlong * cap)()
+        cnts = (ctypes.c_longlong * cap)()
+        _check(lib.sfem_cuda_dist_messages(self.handle, step, chunk, cap, ctypes.byref(ns), ctypes.byref(nr), peers,
+                                           offs, cnts))
+        allm = [(peers[i], offs[i], cnts[i]) for i in range(ns.value + nr.value)]
+        return allm[:ns.value], allm[ns.value:]
 
     def comm_init(self, unique_id: bytes, chunks: int = 0):
         """Create the plan's NCCL communicator from a unique id made by

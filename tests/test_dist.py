@@ -125,6 +125,151 @@ def _gloo_worker(rank, world, port, cfg, out_path):
     dist.destroy_process_group()
 
 
+def _chunked_exchange(r, step, chunks, sendbuf, recvbuf):
+    """One all-to-all of the library-owned schedule over torch.distributed
+    point-to-point messages, chunk by chunk, from the Python restatement of
+    the C++ message lists (dist.chunk_messages)."""
+    from paper_1701_03967_b200.dist import chunk_messages
+    world, rank = dist.get_world_size(), dist.get_rank()
+    for c in range(chunks):
+        sends, recvs = chunk_messages(r.ext, world, rank, chunks, step, c)
+        ops = []
+        for peer, off, cnt in sends:
+            if peer == rank:
+                continue
+            ops.append(dist.P2POp(dist.isend, sendbuf[off:off + cnt], peer))
+        for peer, off, cnt in recvs:
+            if peer == rank:
+                continue
+            ops.append(dist.P2POp(dist.irecv, recvbuf[off:off + cnt], peer))
+        # self messages: matched in order
+        mine_s = [(o, n) for p, o, n in sends if p == rank]
+        mine_r = [(o, n) for p, o, n in recvs if p == rank]
+        assert [n for _, n in mine_s] == [n for _, n in mine_r]
+        for (so, n), (ro, _) in zip(mine_s, mine_r):
+            recvbuf[ro:ro + n] = sendbuf[so:so + n]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+
+def _gloo_chunked_worker(rank, world, port, cfg, chunks, out_path):
+    # the chunked protocol of sfem_cuda_dist_solve with the per-rank phases
+    # emulated by the oracle: x-row chunks packed as [Q][wp_c] blocks at
+    # A + Q*xc0_c, received per (source, chunk) at B + lyR*(x0_s + xc0_{s,c});
+    # exchange 2 per y-row chunk back into the same places
+    from paper_1701_03967_b200.dist import chunk_schedule, padded, partition, partition_even
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orders, elements, lengths, shift = cfg
+        r = OracleRank(orders, elements, lengths, shift, world, rank)
+        ext = r.ext
+        R = r.R
+        Q = ext[1] * R
+        x0s, lxs = partition_even(ext[0], world)
+        y0s, lys = partition(ext[1], world)
+        xc0, xw, yc0, yw = chunk_schedule(ext, world, chunks)
+        lyR = lys[rank] * R
+        nbuf = max(sum(padded(lxs[rank]) * ly * R for ly in lys), sum(padded(lx) * lys[rank] * R for lx in lxs), 2)
+        A = torch.zeros(nbuf, dtype=torch.float64)
+        Bb = torch.zeros(nbuf, dtype=torch.float64)
+        f = np.random.default_rng(99).uniform(-1, 1, ext)
+        x = r.forward_local(f[r.x0:r.x0 + r.lx].copy()).reshape(r.lx, Q)
+        for c in range(chunks):  # PACK1 per x-chunk
+            w = xw[rank][c]
+            if w == 0:
+                continue
+            blk = np.zeros((Q, padded(w)))
+            blk[:, :w] = x[xc0[rank][c]:xc0[rank][c] + w].T
+            A[Q * xc0[rank][c]: Q * xc0[rank][c] + blk.size] = torch.from_numpy(blk.reshape(-1))
+        _chunked_exchange(r, 1, chunks, A, Bb)
+        y = np.zeros((lyR, ext[0]))
+        for s in range(world):  # the axis-0 rows: one segment per (source, chunk)
+            for c in range(chunks):
+                w = xw[s][c]
+                if w == 0 or lyR == 0:
+                    continue
+                pos = x0s[s] + xc0[s][c]
+                y[:, pos:pos + w] = Bb[lyR * pos: lyR * pos + lyR * padded(w)].numpy().reshape(lyR, padded(w))[:, :w]
+        y = r.axis0(y) if lyR > 0 else y
+        for s in range(world):  # back into the same (source, chunk) blocks
+            for c in range(chunks):
+                w = xw[s][c]
+                if w == 0 or lyR == 0:
+                    continue
+                pos = x0s[s] + xc0[s][c]
+                blk = np.zeros((lyR, padded(w)))
+                blk[:, :w] = y[:, pos:pos + w]
+                Bb[lyR * pos: lyR * pos + blk.size] = torch.from_numpy(blk.reshape(-1))
+        _chunked_exchange(r, 2, chunks, Bb, A)
+        xo = np.zeros((r.lx, Q))
+        for c in range(chunks):  # UNPACK2 per x-chunk
+            w = xw[rank][c]
+            if w == 0:
+                continue
+            blk = A[Q * xc0[rank][c]: Q * xc0[rank][c] + Q * padded(w)].numpy().reshape(Q, padded(w))
+            xo[xc0[rank][c]:xc0[rank][c] + w] = blk[:, :w].T
+        xo = r.inverse_local(xo.reshape([r.lx] + ext[1:]))
+        parts = [None] * world
+        dist.all_gather_object(parts, xo)
+        if rank == 0:
+            np.save(out_path, np.concatenate(parts, axis=0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,chunks,cfg", [
+    (2, 2, ([2, 3, 2], [4, 3, 5], [1.0, 1.0, 1.0], 0.5)),
+    (3, 3, ([3, 2], [5, 4], [1.0, 2.0], 0.0)),
+    (2, 4, ([1, 2, 2, 1], [9, 3, 2, 4], [1.0] * 4, 1.0)),
+])
+def test_gloo_chunked_exchange_matches_single_process(tmp_path, world, chunks, cfg):
+    # the N > 1 protocol of sfem_cuda_dist_solve (chunked message lists) over
+    # real multi-process point-to-point messages on CPU
+    out = str(tmp_path / "u.npy")
+    mp.spawn(_gloo_chunked_worker, args=(world, _free_port(), cfg, chunks, out), nprocs=world, join=True)
+    orders, elements, lengths, shift = cfg
+    ext = [n * K - 1 for n, K in zip(orders, elements)]
+    f = np.random.default_rng(99).uniform(-1, 1, ext)
+    want = O.solve_full_diagonalization(f, orders, elements, lengths, shift)
+    assert rel_l2(np.load(out), want) <= 1e-12
+
+
+def test_chunk_message_lists_are_consistent():
+    # every send has a receive of the same size at the peer, in the same order
+    # per pair; offsets stay inside the exchange buffers and never overlap
+    from paper_1701_03967_b200.dist import chunk_messages, padded, partition, partition_even
+    for ext in ([575, 575, 575], [127, 191, 7], [9, 11], [1023, 1023, 1023], [17, 5, 3, 2]):
+        R = int(np.prod(ext[2:])) if len(ext) > 2 else 1
+        for P in (1, 2, 3, 5, 8):
+            if ext[0] < P or ext[1] < P:
+                continue
+            _, lxs = partition_even(ext[0], P)
+            _, lys = partition(ext[1], P)
+            for C in (1, 2, 4):
+                for step in (1, 2):
+                    lists = [[chunk_messages(ext, P, r, C, step, c) for c in range(C)] for r in range(P)]
+                    for r in range(P):
+                        cap = max(sum(padded(lxs[r]) * ly * R for ly in lys), sum(padded(lx) * lys[r] * R for lx in lxs))
+                        for kind in (0, 1):
+                            spans = sorted((o, o + n) for c in range(C) for _, o, n in lists[r][c][kind])
+                            assert all(a2 >= b1 for (_, b1), (a2, _) in zip(spans, spans[1:])), (ext, P, C, step, r)
+                            assert not spans or (spans[0][0] >= 0 and spans[-1][1] <= cap)
+                    for c in range(C):
+                        for src in range(P):
+                            for dst in range(P):
+                                out = [n for p, _, n in lists[src][c][0] if p == dst]
+                                inn = [n for p, _, n in lists[dst][c][1] if p == src]
+                                assert out == inn, (ext, P, C, step, c, src, dst)
+                    # all the data moves: exchange volume = sum over pairs of lxp_src * ly_dst * R
+                    total = sum(n for r in range(P) for c in range(C) for _, _, n in lists[r][c][0])
+                    want = sum(padded(lx) * ly * R for lx in lxs for ly in lys) if step == 1 else None
+                    if step == 1 and C == 1:
+                        assert total == want
+
+
 @pytest.mark.parametrize("world,cfg", [
     (2, ([2, 3, 2], [4, 3, 5], [1.0, 1.0, 1.0], 0.5)),
     (3, ([3, 2], [5, 4], [1.0, 2.0], 0.0)),
@@ -429,3 +574,21 @@ def test_peer_exchange_two_processes_one_gpu_real_ipc():
     for r in range(world):
         assert res[r][0] == 2 * (world - 1) or res[r][0] == 3 * (world - 1), res[r]
     assert all(e <= 1e-13 for e in res[0][1]), res[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,chunks", [(2, 2), (3, 4), (8, 3)])
+def test_chunk_messages_python_mirror_matches_library(sfem, P, chunks):
+    # dist.chunk_messages (used by the CPU gloo test) is the library's own list
+    from paper_1701_03967_b200 import dist as D
+    for orders, elements in (([2, 3, 2], [16, 9, 5]), ([3, 2, 4], [64, 7, 6]), ([9, 9], [64, 64])):
+        spec = sfem.ProblemSpec(len(orders), [1.0] * len(orders), elements, orders, 0.5)
+        for r in range(P):
+            plan = D.DistPlan(spec, P, r)
+            plan.setup(chunks)
+            for step in (1, 2):
+                for c in range(chunks):
+                    got = plan.messages(step, c)
+                    # the library may lower the chunk count (row-segment limit); ask for the same one
+                    want = D.chunk_messages(spec.extents(), P, r, chunks, step, c)
+                    assert got[0] == want[0] and got[1] == want[1], (orders, P, r, step, c)
