@@ -232,6 +232,11 @@ struct Step {
   cuuint32_t sbox[4] = {0, 0, 0, 0};
   const double* smap_ptr = nullptr;
   alignas(64) CUtensorMap smap;
+  // component-major mid tiles (mid_tma_cm): three 5-D maps (sweep.cuh)
+  bool mid_cm = false;
+  long long cm_st_pos = 0, cm_st_outer = 0, cm_ext_outer = 1;  // strides (elements) / extent of the 5-D view
+  const double* cm_ptr = nullptr;
+  alignas(64) CUtensorMap cm_maps[3];
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -255,6 +260,33 @@ void encode4(CUtensorMap* m, const double* data, const cuuint64_t* dims, const c
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// 5-D view {last axis, e >> 1, e & 1, s, outer} of position e * n + s of the swept axis
+void encode5(CUtensorMap* m, const double* data, long long ext0, long long ext1, long long ext2, long long ext3,
+             long long ext4, long long st_pos, long long st_outer, int n, const cuuint32_t* box) {
+  const cuuint64_t dims[5] = {static_cast<cuuint64_t>(ext0), static_cast<cuuint64_t>(ext1), static_cast<cuuint64_t>(ext2),
+                              static_cast<cuuint64_t>(ext3), static_cast<cuuint64_t>(ext4)};
+  const cuuint64_t strides[4] = {static_cast<cuuint64_t>(2 * n * st_pos * 8), static_cast<cuuint64_t>(n * st_pos * 8),
+                                 static_cast<cuuint64_t>(st_pos * 8), static_cast<cuuint64_t>(st_outer * 8)};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(data), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail("cuTensorMapEncodeTiled (5-D) failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+void encode_cm_maps(Step& s, const double* data) {
+  if (s.cm_ptr == data) return;
+  const int n = s.table->dev.n, K = s.table->dev.K;
+  const long long e0 = static_cast<long long>(s.geo.ext0), eo = s.cm_ext_outer;
+  const cuuint32_t boxA[5] = {8u, static_cast<cuuint32_t>(K / 2), 2u, static_cast<cuuint32_t>(n - 1), 1u};
+  const cuuint32_t boxB[5] = {8u, static_cast<cuuint32_t>(K / 2), 1u, 1u, 1u};
+  encode5(&s.cm_maps[0], data, e0, K / 2, 2, n, eo, s.cm_st_pos, s.cm_st_outer, n, boxA);
+  encode5(&s.cm_maps[1], data, e0, K / 2, 2, n, eo, s.cm_st_pos, s.cm_st_outer, n, boxB);
+  // odd elements of the last component: positions (2 e' + 1) n + n - 1, e' < K/2 - 1
+  encode5(&s.cm_maps[2], data + (2 * n - 1) * s.cm_st_pos, e0, K / 2 - 1, 1, 1, eo, s.cm_st_pos, s.cm_st_outer, n, boxB);
+  s.cm_ptr = data;
 }
 
 void encode_map(Step& s, const double* data) {
@@ -419,6 +451,13 @@ Step strided_step(const View& v, int a, int mode) {
     s.box[2] = s.box[3] = 1;
     // L2 prefetch one resident wave ahead where the tile's rows are close (<= 16 KB apart)
     s.geo.prefetch = (st[a] * 8 <= 16384 && mid_tma_prefetch()) ? 2 * 148 : 0;
+    // component-major tiles: one outer axis at most (the 5-D view has no room for two)
+    if (tb == 8 && outer.size() <= 1 && mid_tma_cm(dt.n, dt.K)) {
+      s.mid_cm = true;
+      s.cm_st_pos = st[a];
+      s.cm_st_outer = outer.empty() ? static_cast<long long>(total_bytes / 8) : st[outer.back()];
+      s.cm_ext_outer = outer.empty() ? 1 : v.ext[outer.back()];
+    }
   }
   return s;
 }
@@ -493,6 +532,9 @@ void launch_steps(std::vector<Step>& steps, double* user, sfem_ctx ctx, cudaStre
     } else if (s.tma && aligned) {
       encode_map(s, data);
       ck(launch_sweep_tma(dt, &s.map, nullptr, s.geo, s.mode, kWeighted, stream), "tma sweep launch");
+    } else if (s.mid_tma && s.mid_cm && aligned) {
+      encode_cm_maps(s, data);
+      ck(launch_sweep_mid_tma_cm(dt, s.cm_maps, s.geo, s.mode, kWeighted, stream), "mid tma (component-major) sweep launch");
     } else if (s.mid_tma && aligned) {
       encode_map(s, data);
       ck(launch_sweep_mid_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "mid tma sweep launch");

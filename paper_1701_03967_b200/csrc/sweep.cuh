@@ -179,6 +179,15 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& lines, int mode, 
 int mid_tma_lines(int n, int K);
 cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
                                  cudaStream_t stream);
+// Component-major tiles (sweep_mid_tma_cm, sweep_mid_impl.cuh) for tensors of
+// at most three axes: `maps` are three consecutive CUtensorMaps over the 5-D
+// view {last axis, e >> 1, e & 1, s, outer axis} of position e * n + s:
+// box {8, K/2, 2, n-1, 1}; box {8, K/2, 1, 1, 1}; the same box over the tensor
+// starting at position 2n - 1 with K/2 - 1 entries along the second axis.
+// SFEM_MID_CM=0 turns the layout off (A/B).
+bool mid_tma_cm(int n, int K);
+cudaError_t launch_sweep_mid_tma_cm(const DevTable& t, const void* maps, const TmaGeom& geo, int mode, int analysis,
+                                    cudaStream_t stream);
 
 // Slot-major class tiles (nodal (K+1) x count, interior K*(n-1) x count,
 // [j*count + b]) <-> the slot-major dof tile (n*K-1) x count (lines_block.cu).

@@ -217,6 +217,36 @@ int mid_tma_lines(int n, int K) {
 #endif
 }
 
+// Component-major strided tiles (Cfg::CM): the even orders of the tuned shapes,
+// whose dense 64-byte tile rows keep a warp on one half of the bank line.
+#ifndef SFEM_MID_CM
+#define SFEM_MID_CM 1
+#endif
+bool mid_tma_cm(int n, int K) {
+#if SFEM_MID_CM
+  static const bool on = [] {
+    const char* e = std::getenv("SFEM_MID_CM");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || !mid_tma_enabled()) return false;
+  return (n == 4 && K == 256 && SFEM_MID_B_N4 == 8) || (n == 2 && K == 512 && SFEM_MID_B_N2 == 8);
+#else
+  (void)n;
+  (void)K;
+  return false;
+#endif
+}
+
+cudaError_t launch_sweep_mid_tma_cm(const DevTable& t, const void* maps, const TmaGeom& geo, int mode, int analysis,
+                                    cudaStream_t stream) {
+  if (geo.ntiles <= 0) return cudaSuccess;
+#if SFEM_MID_CM
+  if (t.n == 4 && t.K == 256) return mid::launch_tma_cm<4, 256, 8, SFEM_MID_TH_N4>(t, maps, geo, mode, analysis, stream);
+  if (t.n == 2 && t.K == 512) return mid::launch_tma_cm<2, 512, 8, SFEM_MID_TH_N2>(t, maps, geo, mode, analysis, stream);
+#endif
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
                                  cudaStream_t stream) {
   if (geo.ntiles <= 0) return cudaSuccess;

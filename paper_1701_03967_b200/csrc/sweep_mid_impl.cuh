@@ -69,10 +69,24 @@ using namespace reg;
 // ROWS: tile stored line-major T[b][pos] (line pitch LP, odd: conflict-free
 // for lanes over lines), used when lines are rows of the tensor; otherwise
 // position-major T[pos][b] (strided axes, lanes over the 8 adjacent lines).
-template <int NN, int K, int BB, int TH, bool ROWS_, bool GW = false>
+//
+// CM (strided TMA tiles of 8 lines, n a power of two): component-major tile
+// T[s][e & 1][e >> 1][b] for position e * n + s.  In the dense T[pos][b]
+// layout a tile row is 64 bytes, and both access families of the stages --
+// a warp's items at consecutive frequencies / elements (rows n apart) and at
+// consecutive Makhoul indices (elements 2 apart) -- keep to one half of the
+// 128-byte bank line for even n (C5 n=4: 432M of 1,161M shared wavefronts
+// excess, profiles/r4d_ncu_full_c5n4.json).  Here consecutive elements of one
+// component alternate between two planes and consecutive even (odd) elements
+// are adjacent 64-byte rows, so either family covers whole bank lines.  The
+// TMA unit writes this layout itself (5-D boxes, sweep_mid_tma_cm).
+template <int NN, int K, int BB, int TH, bool ROWS_, bool GW = false, bool CM_ = false>
 struct Cfg {
   static constexpr int n = NN, m = NN - 1, half = m / 2, ne = NN / 2, N = K, L = NN * K - 1;
   static constexpr bool ROWS = ROWS_;
+  static constexpr bool CM = CM_;
+  static_assert(!CM_ || (!ROWS_ && !GW && BB == 8 && (NN & (NN - 1)) == 0 && NN >= 2 && K % 2 == 0),
+                "component-major tiles: strided, 8 lines, n a power of two, even K");
   // PAD (one-line tiles): lanes run ALONG the line, at strides of n or 2n
   // doubles (fills, posts, mixes), i.e. onto 2-4 bank pairs; one pad double
   // per 16 positions spreads 16 consecutive elements / frequencies over all
@@ -87,7 +101,15 @@ struct Cfg {
   static constexpr int LP = PAD ? ((L + (L >> 4) + 1) | 1) : (BULK ? ((LB + 15) / 16 * 16 + 2) : (L | 1));
   static constexpr int PSTR = ROWS ? 1 : BB;  // position stride in the tile (not with PAD: use ix)
   __device__ __forceinline__ static constexpr int ix(int pos, int b) {
+    if (CM) {
+      const int e = pos / NN, s = pos - e * NN;
+      return ((s * 2 + (e & 1)) * (K / 2) + (e >> 1)) * BB + b;
+    }
     return PAD ? pos + (pos >> 4) : (ROWS ? b * LP + pos : pos * BB + b);
+  }
+  // CM: index of component s of element e
+  __device__ __forceinline__ static constexpr int ixe(int e, int s, int b) {
+    return ((s * 2 + (e & 1)) * (K / 2) + (e >> 1)) * BB + b;
   }
   static constexpr int B = BB, Bh = (BB + 1) / 2, Bm = (m & 1) ? Bh : 0;
   static constexpr int NPAIR = B * half;
@@ -103,7 +125,7 @@ struct Cfg {
   static constexpr int J = NPAIR + Bm + ND;
   static constexpr int THREADS = TH;
   static constexpr int WD = 2 * J * K;  // FFT buffer (doubles)
-  static constexpr int TD = ((ROWS || PAD) ? LP : L) * B;  // tile (doubles)
+  static constexpr int TD = CM ? NN * K * B : ((ROWS || PAD) ? LP : L) * B;  // tile (doubles)
   static constexpr int REGION = (GW || TD > WD) ? TD : WD;  // GW: FFT work in global scratch
   static constexpr int NCEN = m * B;  // centre sums
   static constexpr int CHUNKS = NCEN > 0 ? (TH / NCEN > 0 ? TH / NCEN : 1) : 1;
@@ -877,7 +899,9 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
       for (int g = 0; g < G; ++g) {
         const double* pin = Tin + C::ix(m + (k - 1) * n, b0 + g);
 #pragma unroll
-        for (int s = 0; s < n; ++s) v[g][s] = C::PAD ? Tin[C::ix(m + (k - 1) * n + s, b0 + g)] : pin[s * C::PSTR];
+        for (int s = 0; s < n; ++s)
+          v[g][s] = C::CM ? Tin[C::ixe(k - 1 + (s > 0), s > 0 ? s - 1 : n - 1, b0 + g)]
+                          : (C::PAD ? Tin[C::ix(m + (k - 1) * n + s, b0 + g)] : pin[s * C::PSTR]);
       }
       if (MODE != kInverse) {
 #if SFEM_MID_KMIX
@@ -939,14 +963,18 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
 #endif
           double* p = T + C::ix(m + (k - 1) * n, b0 + g);
 #pragma unroll
-          for (int s = 0; s < n; ++s) (C::PAD ? T[C::ix(m + (k - 1) * n + s, b0 + g)] : p[s * C::PSTR]) = v[g][s];
+          for (int s = 0; s < n; ++s)
+            (C::CM ? T[C::ixe(k - 1 + (s > 0), s > 0 ? s - 1 : n - 1, b0 + g)]
+                   : (C::PAD ? T[C::ix(m + (k - 1) * n + s, b0 + g)] : p[s * C::PSTR])) = v[g][s];
         }
       } else {
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           double* p = T + C::ix(m + (k - 1) * n, b0 + g);
 #pragma unroll
-          for (int l = 0; l < n; ++l) (C::PAD ? T[C::ix(m + (k - 1) * n + l, b0 + g)] : p[l * C::PSTR]) = c[g][l];
+          for (int l = 0; l < n; ++l)
+            (C::CM ? T[C::ixe(k - 1 + (l > 0), l > 0 ? l - 1 : n - 1, b0 + g)]
+                   : (C::PAD ? T[C::ix(m + (k - 1) * n + l, b0 + g)] : p[l * C::PSTR])) = c[g][l];
         }
       }
     } else if (m > 0) {
@@ -1515,6 +1543,164 @@ cudaError_t launch_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, 
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TS::SMEM));
       if (err != cudaSuccess) return err;
       kern<<<grid, TH, TS::SMEM, stream>>>(t, *map, geo, mixF, e0F);
+    }
+    return cudaGetLastError();
+  }
+}
+
+// Component-major tiles (Cfg::CM) by 5-D tensor copies.  The tensor is viewed
+// as {last axis, e >> 1, e & 1, s, outer axis} for position e * n + s of the
+// swept axis, so one box {8, K/2, 2, n-1, 1} lands as the planes [s][e & 1] of
+// components s < n-1; the last component's planes (the line has no position
+// n K - 1) come by two boxes {8, K/2, 1, 1, 1}: even elements through mapB,
+// odd ones through mapC, whose tensor ends one element early so the TMA unit
+// clips the missing position (zero-filled on load, skipped on store).
+template <int NN, int K, int BB, int TH>
+struct TmaShapeCM {
+  using C = Cfg<NN, K, BB, TH, false, false, true>;
+  static constexpr bool OK = BB == 8 && NN >= 2 && K / 2 <= 256 && NN * K * BB <= C::REGION;
+  static constexpr int PLANE = (K / 2) * BB;  // doubles per [s][e & 1] plane
+  static constexpr int BAR_OFF = (C::TOTAL + 1) & ~1;
+  static constexpr size_t SMEM = static_cast<size_t>(BAR_OFF + 2) * sizeof(double);
+};
+
+template <int NN, int K, int BB, int TH, int MODE>
+__global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))
+    sweep_mid_tma_cm(DevTable t, const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                     const __grid_constant__ CUtensorMap mapC, TmaGeom geo, const double* __restrict__ mixF,
+                     const double* __restrict__ e0F) {
+  using C = Cfg<NN, K, BB, TH, false, false, true>;
+  using TS = TmaShapeCM<NN, K, BB, TH>;
+  extern __shared__ __align__(128) double smem[];
+  double* R = smem;
+  double* C0 = smem + C::C0_OFF;
+  double* PS = smem + C::PS_OFF;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + TS::BAR_OFF);
+  SFEM_PT_DECL;
+  SFEM_PT(0);
+  int c0, c2;
+  if (gridDim.y > 1 || geo.ntiles == geo.nblk0) {
+    c0 = static_cast<int>(blockIdx.x) * BB;
+    c2 = static_cast<int>(blockIdx.y);
+  } else {
+    const long long tile = blockIdx.x;
+    c0 = static_cast<int>(tile % geo.nblk0) * BB;
+    c2 = static_cast<int>(tile / geo.nblk0);
+  }
+  double* RB = R + (NN - 1) * 2 * TS::PLANE;  // planes of the last component
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mid_smem_u32(bar)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mid_smem_u32(bar)),
+                 "r"(static_cast<unsigned>(NN * 2 * TS::PLANE * sizeof(double)))
+                 : "memory");
+    if (NN > 1)
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+          "%6}], [%7];\n" ::"r"(mid_smem_u32(R)),
+          "l"(&mapA), "r"(c0), "r"(0), "r"(0), "r"(0), "r"(c2), "r"(mid_smem_u32(bar))
+          : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];\n" ::"r"(mid_smem_u32(RB)),
+        "l"(&mapB), "r"(c0), "r"(0), "r"(0), "r"(NN - 1), "r"(c2), "r"(mid_smem_u32(bar))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];\n" ::"r"(mid_smem_u32(RB + TS::PLANE)),
+        "l"(&mapC), "r"(c0), "r"(0), "r"(0), "r"(0), "r"(c2), "r"(mid_smem_u32(bar))
+        : "memory");
+    if (geo.prefetch > 0) {
+      const long long lin = static_cast<long long>(c2) * geo.nblk0 + c0 / BB;
+      const long long nxt = lin + geo.prefetch;
+      if (nxt < geo.ntiles) {
+        const int p0 = static_cast<int>(nxt % geo.nblk0) * BB, p2 = static_cast<int>(nxt / geo.nblk0);
+        if (NN > 1)
+          asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(&mapA), "r"(p0),
+                       "r"(0), "r"(0), "r"(0), "r"(p2)
+                       : "memory");
+        asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(&mapB), "r"(p0),
+                     "r"(0), "r"(0), "r"(NN - 1), "r"(p2)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(&mapC), "r"(p0),
+                     "r"(0), "r"(0), "r"(0), "r"(p2)
+                     : "memory");
+      }
+    }
+  }
+  __syncthreads();  // the barrier is initialised before anyone polls it
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(mid_smem_u32(bar)),
+      "r"(0)
+      : "memory");
+  SFEM_PT(1);
+  SymbolInfo nosym{};
+  if (MODE != kInverse) {
+    forward_fft_inplace<C>(R, PS, t.tw, t.om);
+    centre_reduce<C>(PS, C0);
+    forward_post<C>(reinterpret_cast<const double2*>(R), R, t.mk);
+  }
+  SFEM_PT(2);
+  mix<C, MODE>(R, R, C0, mixF, e0F, SFEM_MID_KMIX ? t.mixT_i : t.mix_inv, t.e0_inv, nullptr, t.eig, nosym.f_last);
+  SFEM_PT(3);
+  if (MODE != kForward) {
+    inverse_fft_inplace<C>(R, t.tw, t.mkh, t.om);
+    inverse_post<C>(reinterpret_cast<const double2*>(R), R, C0);
+  }
+  SFEM_PT(4);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (NN > 1)
+      asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(&mapA),
+                   "r"(c0), "r"(0), "r"(0), "r"(0), "r"(c2), "r"(mid_smem_u32(R))
+                   : "memory");
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(&mapB),
+                 "r"(c0), "r"(0), "r"(0), "r"(NN - 1), "r"(c2), "r"(mid_smem_u32(RB))
+                 : "memory");
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(&mapC),
+                 "r"(c0), "r"(0), "r"(0), "r"(0), "r"(c2), "r"(mid_smem_u32(RB + TS::PLANE))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  }
+  SFEM_PT(5);
+  SFEM_PT_FLUSH(30 + MODE);
+}
+
+// maps[0..2] = mapA, mapB, mapC (64-byte aligned CUtensorMaps)
+template <int NN, int K, int BB, int TH>
+cudaError_t launch_tma_cm(const DevTable& t, const void* maps, const TmaGeom& geo, int mode, int analysis,
+                          cudaStream_t stream) {
+  using TS = TmaShapeCM<NN, K, BB, TH>;
+  if constexpr (!TS::OK) {
+    return cudaErrorNotSupported;
+  } else {
+    if (mode == kForwardDivideInverse) return cudaErrorInvalidValue;
+    const double* mixF = SFEM_MID_KMIX ? (analysis == kDirect ? t.mixT_d : t.mixT_w)
+                                       : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
+    const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
+    const CUtensorMap* map = static_cast<const CUtensorMap*>(maps);
+    const long long rest = geo.ntiles / geo.nblk0;
+    const bool grid2 = geo.nblk0 < (1LL << 31) && rest <= 65535;
+    const dim3 grid = grid2 ? dim3(static_cast<unsigned>(geo.nblk0), static_cast<unsigned>(rest))
+                            : dim3(static_cast<unsigned>(geo.ntiles));
+    cudaError_t err;
+    if (mode == kForward) {
+      auto kern = sweep_mid_tma_cm<NN, K, BB, TH, kForward>;
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TS::SMEM));
+      if (err != cudaSuccess) return err;
+      kern<<<grid, TH, TS::SMEM, stream>>>(t, map[0], map[1], map[2], geo, mixF, e0F);
+    } else {
+      auto kern = sweep_mid_tma_cm<NN, K, BB, TH, kInverse>;
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TS::SMEM));
+      if (err != cudaSuccess) return err;
+      kern<<<grid, TH, TS::SMEM, stream>>>(t, map[0], map[1], map[2], geo, mixF, e0F);
     }
     return cudaGetLastError();
   }
