@@ -111,6 +111,10 @@ struct Cfg {
   __device__ __forceinline__ static constexpr int ixe(int e, int s, int b) {
     return ((s * 2 + (e & 1)) * (K / 2) + (e >> 1)) * BB + b;
   }
+  // position e * n + c (0 <= c < n) given as element and component
+  __device__ __forceinline__ static constexpr int ixp(int e, int c, int b) {
+    return CM ? ixe(e, c, b) : ix(e * NN + c, b);
+  }
   static constexpr int B = BB, Bh = (BB + 1) / 2, Bm = (m & 1) ? Bh : 0;
   static constexpr int NPAIR = B * half;
   // PK (one-line tiles, m odd; C2's n = 4, K = 4096): the middle job's second
@@ -129,7 +133,9 @@ struct Cfg {
   static constexpr int REGION = (GW || TD > WD) ? TD : WD;  // GW: FFT work in global scratch
   static constexpr int NCEN = m * B;  // centre sums
   static constexpr int CHUNKS = NCEN > 0 ? (TH / NCEN > 0 ? TH / NCEN : 1) : 1;
-  static constexpr int ECH = (K + CHUNKS - 1) / CHUNKS;  // elements per chunk
+  // elements per chunk; CM: twice an odd count, so the chunks of the lanes of a warp start in alternate bank halves
+  static constexpr int ECH0 = (K + CHUNKS - 1) / CHUNKS;
+  static constexpr int ECH = CM ? (((ECH0 + 1) / 2) | 1) * 2 : ECH0;
   static constexpr int C0_OFF = REGION;
   static constexpr int PS_OFF = C0_OFF + (NCEN > 0 ? NCEN : 1);
   static constexpr int BASE_OFF = PS_OFF + (NCEN > 0 ? CHUNKS * NCEN : 1);
@@ -561,26 +567,26 @@ __device__ __forceinline__ void forward_fill(const double* T, double* R, double*
       if (job < NPAIR) {
         const int ii = job / B, b = job % B;
         const int e = makhoul_src(tt, N);
-        const double ri = T[C::ix(e * n + ii, b)], rr = T[C::ix(e * n + m - 1 - ii, b)];
+        const double ri = T[C::ixp(e, ii, b)], rr = T[C::ixp(e, m - 1 - ii, b)];
         double gg = ri + rr;
         if (e & 1) gg = -gg;
         z[i] = make_double2(ri - rr, gg);
       } else if (job < NPAIR + C::Bm) {
         const int b = job - NPAIR, b2 = b + Bh;
         const int e = makhoul_src(tt, N);
-        double g1 = T[C::ix(e * n + C::half, b)];
-        double g2 = b2 < B ? T[C::ix(e * n + C::half, b2)] : 0.0;
+        double g1 = T[C::ixp(e, C::half, b)];
+        double g2 = b2 < B ? T[C::ixp(e, C::half, b2)] : 0.0;
         if (e & 1) {
           g1 = -g1;
           g2 = -g2;
         }
-        if (C::PK) g2 = tt > 0 ? T[C::ix(tt * n - 1, b)] : 0.0;  // nodal values (even-index DST-I half)
+        if (C::PK) g2 = tt > 0 ? T[C::ixp(tt - 1, n - 1, b)] : 0.0;  // nodal values (even-index DST-I half)
         z[i] = make_double2(g1, g2);
       } else {
         const int jb = job - NPAIR - C::Bm;
         const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, b2 = b + Bh;
         if (tt > 0) {
-          z[i] = make_double2(T[C::ix(tt * n - 1, b)], b2 < B ? T[C::ix(tt * n - 1, b2)] : 0.0);
+          z[i] = make_double2(T[C::ixp(tt - 1, n - 1, b)], b2 < B ? T[C::ixp(tt - 1, n - 1, b2)] : 0.0);
           if (which) z[i] = c_mul(z[i], __ldg(om + tt));
         }
       }
@@ -595,7 +601,7 @@ __device__ __forceinline__ void forward_fill(const double* T, double* R, double*
       const int s = cit % C::NCEN, c = cit / C::NCEN;
       const int ii = s / B, b = s % B;
       const int e0 = c * C::ECH, e1 = min(N, e0 + C::ECH);
-      for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ix(e * n + m - 1 - ii, b)] : T[C::ix(e * n + ii, b)];
+      for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ixp(e, m - 1 - ii, b)] : T[C::ixp(e, ii, b)];
     }
   }
   if (!SEP) {
@@ -627,26 +633,26 @@ __device__ __forceinline__ double2 forward_elem(const double* T, int job, int tt
   if (job < NPAIR) {
     const int ii = job / B, b = job % B;
     const int e = makhoul_src(tt, N);
-    const double ri = T[C::ix(e * n + ii, b)], rr = T[C::ix(e * n + m - 1 - ii, b)];
+    const double ri = T[C::ixp(e, ii, b)], rr = T[C::ixp(e, m - 1 - ii, b)];
     double gg = ri + rr;
     if (e & 1) gg = -gg;
     z = make_double2(ri - rr, gg);
   } else if (job < NPAIR + C::Bm) {
     const int b = job - NPAIR, b2 = b + Bh;
     const int e = makhoul_src(tt, N);
-    double g1 = T[C::ix(e * n + C::half, b)];
-    double g2 = b2 < B ? T[C::ix(e * n + C::half, b2)] : 0.0;
+    double g1 = T[C::ixp(e, C::half, b)];
+    double g2 = b2 < B ? T[C::ixp(e, C::half, b2)] : 0.0;
     if (e & 1) {
       g1 = -g1;
       g2 = -g2;
     }
-    if (C::PK) g2 = tt > 0 ? T[C::ix(tt * n - 1, b)] : 0.0;
+    if (C::PK) g2 = tt > 0 ? T[C::ixp(tt - 1, n - 1, b)] : 0.0;
     z = make_double2(g1, g2);
   } else {
     const int jb = job - NPAIR - C::Bm;
     const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, b2 = b + Bh;
     if (tt > 0) {
-      z = make_double2(T[C::ix(tt * n - 1, b)], b2 < B ? T[C::ix(tt * n - 1, b2)] : 0.0);
+      z = make_double2(T[C::ixp(tt - 1, n - 1, b)], b2 < B ? T[C::ixp(tt - 1, n - 1, b2)] : 0.0);
       if (which) z = c_mul(z, __ldg(om + tt));
     }
   }
@@ -659,12 +665,14 @@ __device__ __forceinline__ void centre_partials(const double* T, double* PS) {
   if constexpr (C::NCEN > 0) {
     const int cit = threadIdx.x;
     if (cit < C::CHUNKS * C::NCEN) {
-      const int s = cit % C::NCEN, c = cit / C::NCEN;
+      // CM: a warp covers four consecutive chunks of one component (rows of one plane pair)
+      const int s = C::CM ? (cit / (B * C::CHUNKS)) * B + cit % B : cit % C::NCEN;
+      const int c = C::CM ? (cit / B) % C::CHUNKS : cit / C::NCEN;
       const int ii = s / B, b = s % B;
       const int e0 = c * C::ECH, e1 = min(N, e0 + C::ECH);
       double part = 0.0;
-      for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ix(e * n + m - 1 - ii, b)] : T[C::ix(e * n + ii, b)];
-      PS[cit] = part;
+      for (int e = e0; e < e1; ++e) part += (e & 1) ? -T[C::ixp(e, m - 1 - ii, b)] : T[C::ixp(e, ii, b)];
+      PS[c * C::NCEN + s] = part;
     }
   }
 }
@@ -758,17 +766,17 @@ __device__ __forceinline__ Out2 forward_post_item(const double2* Z, int it, cons
     o.v2 = w.x * a2 - w.y * b2;
     if (job < NPAIR) {
       const int ii = job / B, b = job % B;
-      o.i1 = C::ix(m + (k - 1) * n + 1 + C::ne + ii, b);  // H_k
-      o.i2 = C::ix(m + (N - k - 1) * n + 1 + ii, b);      // G_{N-k}
+      o.i1 = C::ixp(k, C::ne + ii, b);  // H_k
+      o.i2 = C::ixp(N - k, ii, b);      // G_{N-k}
     } else {
       const int b = job - NPAIR, bb = b + Bh;
-      o.i1 = C::ix(m + (N - k - 1) * n + 1 + C::half, b);
-      if (bb < B) o.i2 = C::ix(m + (N - k - 1) * n + 1 + C::half, bb);
+      o.i1 = C::ixp(N - k, C::half, b);
+      if (bb < B) o.i2 = C::ixp(N - k, C::half, bb);
       if (C::PK && (k & 1) == 0) {
         // even nodal frequency k = 2 kp from the imaginary payload
         const int kp = k / 2;
         o.v2 = 0.5 * (Z[kp * J + job].x - Z[(N - kp) * J + job].x);
-        o.i2 = C::ix(m + (k - 1) * n, b);
+        o.i2 = C::ixp(k - 1, n - 1, b);
       }
     }
   } else {
@@ -786,8 +794,8 @@ __device__ __forceinline__ Out2 forward_post_item(const double2* Z, int it, cons
       // X = d / (2i)
       o.v1 = 0.5 * d.y;
       o.v2 = -0.5 * d.x;
-      o.i1 = C::ix(m + (k - 1) * n, b);
-      if (bb < B) o.i2 = C::ix(m + (k - 1) * n, bb);
+      o.i1 = C::ixp(k - 1, n - 1, b);
+      if (bb < B) o.i2 = C::ixp(k - 1, n - 1, bb);
     }
   }
   return o;
@@ -992,11 +1000,11 @@ __device__ __forceinline__ void mix(const double* Tin, double* T, double* C0, co
         }
       } else {
 #pragma unroll
-        for (int l = 0; l < m; ++l) c[l] = Tin[C::ix(l, b)];
+        for (int l = 0; l < m; ++l) c[l] = Tin[C::ixp(0, l, b)];
       }
       if (MODE == kForward) {
 #pragma unroll
-        for (int l = 0; l < m; ++l) T[C::ix(l, b)] = c[l];
+        for (int l = 0; l < m; ++l) T[C::ixp(0, l, b)] = c[l];
       } else {
         // centre of the synthesis: C0[i] = sum_l e0_inv[i][l] c[l]
 #pragma unroll
@@ -1039,16 +1047,16 @@ __device__ __forceinline__ double2 inverse_elem(const double* T, int job, int tt
       double ax, ar, bx, br;  // V1 = w (ax - i ar), V2 = w (bx - i br)
       if (job < NPAIR) {
         const int ii = job / B, b = job % B;
-        ax = T[C::ix(m + (tt - 1) * n + 1 + C::ne + ii, b)];
-        ar = T[C::ix(m + (N - tt - 1) * n + 1 + C::ne + ii, b)];
-        bx = T[C::ix(m + (N - tt - 1) * n + 1 + ii, b)];
-        br = T[C::ix(m + (tt - 1) * n + 1 + ii, b)];
+        ax = T[C::ixp(tt, C::ne + ii, b)];
+        ar = T[C::ixp(N - tt, C::ne + ii, b)];
+        bx = T[C::ixp(N - tt, ii, b)];
+        br = T[C::ixp(tt, ii, b)];
       } else {
         const int b = job - NPAIR, b2 = b + Bh;
-        ax = T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b)];
-        ar = T[C::ix(m + (tt - 1) * n + 1 + C::half, b)];
-        bx = b2 < B ? T[C::ix(m + (N - tt - 1) * n + 1 + C::half, b2)] : 0.0;
-        br = b2 < B ? T[C::ix(m + (tt - 1) * n + 1 + C::half, b2)] : 0.0;
+        ax = T[C::ixp(N - tt, C::half, b)];
+        ar = T[C::ixp(tt, C::half, b)];
+        bx = b2 < B ? T[C::ixp(N - tt, C::half, b2)] : 0.0;
+        br = b2 < B ? T[C::ixp(tt, C::half, b2)] : 0.0;
       }
       const double2 v1 = c_mul(w, make_double2(ax, -ar));
       const double2 v2 = c_mul(w, make_double2(bx, -br));
@@ -1057,12 +1065,12 @@ __device__ __forceinline__ double2 inverse_elem(const double* T, int job, int tt
       if (C::PK && job >= NPAIR) {
         // + (s_t - s_{N-t}) / 2 (antisymmetric, real): its inverse DFT is i * sum_t s_t sin(2 pi t j / N)
         const int b = job - NPAIR;
-        z.x += 0.5 * (T[C::ix(m + (tt - 1) * n, b)] - T[C::ix(m + (N - tt - 1) * n, b)]);
+        z.x += 0.5 * (T[C::ixp(tt - 1, n - 1, b)] - T[C::ixp(N - tt - 1, n - 1, b)]);
       }
     } else {
       const int jb = job - NPAIR - C::Bm;
       const int b = jb % Bh, which = C::PK ? 1 : jb / Bh, b2 = b + Bh;
-      z = make_double2(T[C::ix(m + (tt - 1) * n, b)], b2 < B ? T[C::ix(m + (tt - 1) * n, b2)] : 0.0);
+      z = make_double2(T[C::ixp(tt - 1, n - 1, b)], b2 < B ? T[C::ixp(tt - 1, n - 1, b2)] : 0.0);
       if (which) z = c_mul(z, __ldg(om + tt));
     }
   }
@@ -1137,18 +1145,18 @@ __device__ __forceinline__ Out2 inverse_post_item(const double2* Z, int it, cons
       const double cr = odd ? -C0[ii * B + b] : C0[(m - 1 - ii) * B + b];
       o.v1 = ci + ev + ure;
       o.v2 = cr + ev - ure;
-      o.i1 = C::ix(e * n + ii, b);
-      o.i2 = C::ix(e * n + m - 1 - ii, b);
+      o.i1 = C::ixp(e, ii, b);
+      o.i2 = C::ixp(e, m - 1 - ii, b);
     } else {
       const int b = job - NPAIR, b2 = b + Bh;
       constexpr int hc = C::half;
       const double c1 = odd ? -C0[hc * B + b] : C0[hc * B + b];
       o.v1 = c1 + (odd ? -ure : ure);
-      o.i1 = C::ix(e * n + hc, b);
+      o.i1 = C::ixp(e, hc, b);
       if (b2 < B) {
         const double c2 = odd ? -C0[hc * B + b2] : C0[hc * B + b2];
         o.v2 = c2 + (odd ? -uim : uim);
-        o.i2 = C::ix(e * n + hc, b2);
+        o.i2 = C::ixp(e, hc, b2);
       }
       if (C::PK && tt >= 1 && 2 * tt <= N - 1) {
         o.v2 = uim;  // node 2 tt
@@ -1169,10 +1177,10 @@ __device__ __forceinline__ Out2 inverse_post_item(const double2* Z, int it, cons
         d = c_sub(Z[(N - 1 - kp) * J + job], Z[kp * J + job]);
       }
       o.v1 = 0.5 * d.y;
-      o.i1 = C::ix(j * n - 1, b);
+      o.i1 = C::ixp(j - 1, n - 1, b);
       if (b2 < B) {
         o.v2 = -0.5 * d.x;
-        o.i2 = C::ix(j * n - 1, b2);
+        o.i2 = C::ixp(j - 1, n - 1, b2);
       }
     }
   }
