@@ -610,6 +610,9 @@ class Plan:
         _check(lib.sfem_cuda_solve_host_batch(self.handle, len(loads), ptrs(loads), ptrs(outs)))
 
     def solve_device(self, dev_ptr: int, pitch: Optional[int] = None, stream: int = 0):
+        """sfem_cuda_solve_device, in place.  stream 0 = the context's own non-blocking stream: work queued on
+        another stream (e.g. torch's current one filling the tensor) is NOT ordered before the solve -- synchronise
+        first or pass that stream (torch.cuda.current_stream().cuda_stream)."""
         _check(lib.sfem_cuda_solve_device(self.handle, ctypes.c_void_p(dev_ptr),
                                           self.pitch if pitch is None else pitch, ctypes.c_void_p(stream or None)))
 

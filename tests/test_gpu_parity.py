@@ -181,6 +181,8 @@ def test_random_solves_match_oracle(sfem, orders, elements, lengths, shift):
     ([1, 2, 2], [1024, 3, 5]),   # n = 1 four-line tiles, 9 last-axis dofs = 2 full tiles + 1 line
     ([2, 2, 1, 4], [2, 512, 3, 2]),   # 4-D: K = 512 strided with two outer axes
     ([9, 2], [1024, 4]),         # C3's two-line tiles, 7 last-axis dofs (odd)
+    ([4, 2, 3], [256, 512, 4]),  # component-major tiles (5-D tensor copies) on both strided axes, 11 last-axis dofs
+    ([2, 3], [512, 5]),          # component-major n = 2 tiles, 2-D (no outer axis), 14 last-axis dofs
 ])
 def test_mid_tma_tiles_ragged_shapes(sfem, orders, elements, monkeypatch):
     # strided sweeps with TMA tiles (sweep_mid_tma): partial tiles rely on the

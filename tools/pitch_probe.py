@@ -25,6 +25,7 @@ for pad in a.pads:
     g = torch.Generator(device="cuda").manual_seed(0)
     buf = torch.rand(rows, pitch, dtype=torch.float64, device="cuda", generator=g) - 0.5
     x = buf.clone()
+    torch.cuda.synchronize()  # the plan runs on its own non-blocking stream
     plan.solve_device(x.data_ptr(), pitch)
     torch.cuda.synchronize()
     chk = float(x[:, : plan.extents[-1]].norm())

@@ -64,6 +64,8 @@ CASES = {
     # compile-time mid kernels (cp.async tiles, Stockham passes)
     "mid2d": lambda: solve_case("mid2d", [4, 2], [256, 128], 0.5),
     "mid3d": lambda: solve_case("mid3d", [2, 1, 3], [32, 128, 16], 0.5),
+    # component-major strided tiles by 5-D tensor copies (n = 2 / K = 512 and n = 4 / K = 256), ragged last axis
+    "midcm3d": lambda: solve_case("midcm3d", [2, 4, 3], [512, 256, 4], 0.5),
     # runtime-radix generic kernels
     "generic": lambda: solve_case("generic", [3, 2], [14, 22]),
     # 1D line API (persistent K = 64 kernel, mid kernel, generic)
