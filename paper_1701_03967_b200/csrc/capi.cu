@@ -535,6 +535,12 @@ void launch_steps(std::vector<Step>& steps, double* user, sfem_ctx ctx, cudaStre
     } else if (s.mid_tma && s.mid_cm && aligned) {
       encode_cm_maps(s, data);
       ck(launch_sweep_mid_tma_cm(dt, s.cm_maps, s.geo, s.mode, kWeighted, stream), "mid tma (component-major) sweep launch");
+    } else if (s.mid_tma && aligned && (data != dst || s.geo.ld_mode != kBoxPlain)) {  // blocked schedule (mid)
+      require(reinterpret_cast<unsigned long long>(dst) % 16 == 0, "blocked sweep: unaligned tensor");
+      encode_map(s, data);
+      if (data != dst) encode_smap(s, dst);
+      ck(launch_sweep_mid_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream, data != dst ? &s.smap : nullptr),
+         "mid tma sweep launch (blocked)");
     } else if (s.mid_tma && aligned) {
       encode_map(s, data);
       ck(launch_sweep_mid_tma(dt, &s.map, s.geo, s.mode, kWeighted, stream), "mid tma sweep launch");
@@ -734,11 +740,105 @@ void build_blocked_steps(sfem_plan_s* p, long long pitch) {
   p->blocked = true;
 }
 
+// The same schedule for the mid kernels (sweep_mid_tma with box modes, sweep_mid rows with the blocked row
+// order in the symbol): shapes mid_tma_blocked() names, all three axes on one table.
+bool blocked_mid_ok(const sfem_plan_s* p, long long pitch) {
+  if (p->dim != 3 || !p->use_fast || std::getenv("SFEM_PLAIN")) return false;
+  const DevTable& t0 = p->tables[0]->dev;
+  if (p->tables[1] != p->tables[0] || p->tables[2] != p->tables[0]) return false;
+  if (!mid_tma_blocked(t0.n, t0.K) || mid_tma_lines(t0.n, t0.K) <= 0 || mid_tma_cm(t0.n, t0.K)) return false;
+  const long long nhi = (p->ext[0] + kXBlk - 1) / kXBlk;
+  const long long tb = mid_tma_lines(t0.n, t0.K), nbox = (p->ext[0] + 255) / 256;
+  const long long balign = tb % 16 == 0 ? 1 : (tb % 8 == 0 ? 2 : (tb % 4 == 0 ? 4 : (tb % 2 == 0 ? 8 : 16)));
+  const long long boxp = ((p->ext[0] + nbox - 1) / nbox + balign - 1) / balign * balign;  // as strided_step
+  // one box {lines, xblk, nhi, 1} must fill exactly the region the nbox plain boxes fill
+  return nhi <= 256 && kXBlk * nhi == nbox * boxp && (pitch * 8) % 16 == 0 && p->ext[2] >= 2;
+}
+
+void build_blocked_mid_steps(sfem_plan_s* p, long long pitch) {
+  const long long L0 = p->ext[0], L1 = p->ext[1], L2 = p->ext[2];
+  const long long bp = (L2 + 3) & ~3LL, X = kXBlk, nhi = (L0 + X - 1) / X;
+  p->bpitch = bp;
+  p->belems = static_cast<size_t>(nhi) * X * L1 * bp;
+  const View v = plan_view(p, pitch);
+  const cuuint64_t sxlo = bp * 8, sy = X * bp * 8, sxhi = L1 * X * bp * 8;
+  auto axis1 = [&](int mode) {
+    Step s = strided_step(v, 1, mode);  // plain geometry: d0 z, d1 y (swept), d2 x
+    require(s.mid_tma && !s.mid_cm, "blocked schedule (mid): axis-1 TMA step");
+    for (int i = 0; i < 4; ++i) s.sdims[i] = s.dims[i], s.sbox[i] = s.box[i];
+    for (int i = 0; i < 3; ++i) s.sstrides[i] = s.strides[i];
+    // the blocked side: {z, y, x_lo, x_hi}, the tile's x split
+    cuuint64_t* bd = mode == kForward ? s.sdims : s.dims;
+    cuuint64_t* bs = mode == kForward ? s.sstrides : s.strides;
+    bd[0] = L2;
+    bd[1] = L1;
+    bd[2] = X;
+    bd[3] = nhi;
+    bs[0] = sy;
+    bs[1] = sxlo;
+    bs[2] = sxhi;
+    s.geo.xblk = X;
+    s.geo.ld_mode = mode == kForward ? kBoxPlain : kBoxSplit;
+    s.geo.st_mode = mode == kForward ? kBoxSplit : kBoxPlain;
+    s.src_buf = mode == kForward ? 0 : 1;
+    s.dst_buf = mode == kForward ? 1 : 0;
+    return s;
+  };
+  auto axis0 = [&](int mode) {
+    Step s = strided_step(v, 0, mode);  // table / line set of axis 0; geometry replaced
+    require(s.mid_tma && !s.mid_cm, "blocked schedule (mid): axis-0 TMA step");
+    const long long tb = s.box[0];
+    s.dims[0] = L2;
+    s.dims[1] = X;
+    s.dims[2] = nhi;
+    s.dims[3] = L1;
+    s.strides[0] = sxlo;
+    s.strides[1] = sxhi;
+    s.strides[2] = sy;
+    s.box[1] = static_cast<cuuint32_t>(X);
+    s.box[2] = static_cast<cuuint32_t>(nhi);
+    s.box[3] = 1;
+    s.geo.nblk0 = (L2 + tb - 1) / tb;
+    s.geo.ext0 = L2;
+    s.geo.ext2 = L1;
+    s.geo.ntiles = s.geo.nblk0 * L1;
+    s.geo.xblk = X;
+    s.geo.ld_mode = s.geo.st_mode = kBoxSwept;
+    s.geo.prefetch = 0;
+    s.src_buf = s.dst_buf = 1;
+    return s;
+  };
+  Step rows = rows_step(v, kForwardDivideInverse);
+  rows.ls.nlines = nhi * L1 * X;
+  rows.ls.n1 = rows.ls.nlines;
+  rows.ls.os1 = bp;
+  rows.bulk_rows = false;
+  SymbolInfo& sy_ = rows.sym;
+  sy_.nlead = 3;
+  sy_.lead_ext[0] = nhi;
+  sy_.lead_ext[1] = L1;
+  sy_.lead_ext[2] = X;
+  sy_.xblk = static_cast<int>(X);
+  sy_.x_ext = L0;
+  rows.src_buf = rows.dst_buf = 1;
+  p->steps.clear();
+  p->steps.push_back(axis1(kForward));
+  p->steps.push_back(axis0(kForward));
+  p->steps.push_back(rows);
+  p->steps.push_back(axis0(kInverse));
+  p->steps.push_back(axis1(kInverse));
+  p->blocked = true;
+}
+
 void build_steps(sfem_plan_s* p, long long pitch) {
   const int N = p->dim;
   p->blocked = false;
   if (blocked_ok(p, pitch)) {
     build_blocked_steps(p, pitch);
+    return;
+  }
+  if (blocked_mid_ok(p, pitch)) {
+    build_blocked_mid_steps(p, pitch);
     return;
   }
   const View v = plan_view(p, pitch);

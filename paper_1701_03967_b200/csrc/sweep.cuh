@@ -177,8 +177,11 @@ cudaError_t launch_sweep_mid(const DevTable& t, const LineSet& lines, int mode, 
 // {last axis, swept axis, outer, outer} with box {lines, geo.boxp, 1, 1};
 // geo.nblk0 counts tiles of `lines` last-axis indices.  In place.
 int mid_tma_lines(int n, int K);
+// `smap` (blocked 3-D schedule of the shapes mid_tma_blocked() names): the map the tile is stored through when
+// it differs from `tmap`; geo.ld_mode / st_mode / xblk give the box coordinates of either side (BoxMode).
 cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, const void* smap = nullptr);
+bool mid_tma_blocked(int n, int K);
 // Component-major tiles (sweep_mid_tma_cm, sweep_mid_impl.cuh) for tensors of
 // at most three axes: `maps` are three consecutive CUtensorMaps over the 5-D
 // view {last axis, e >> 1, e & 1, s, outer axis} of position e * n + s:

@@ -247,11 +247,24 @@ cudaError_t launch_sweep_mid_tma_cm(const DevTable& t, const void* maps, const T
   return cudaErrorNotSupported;
 }
 
+// Shapes whose 3-D solves run the blocked schedule (capi.cu build_blocked_mid_steps): axis 0 stored as
+// (x_hi, y, x_lo, z) in a plan scratch, so an axis-0 tile's rows are 8-row groups instead of one row per plane.
+// n = 1, K = 1024 (C5): 32-byte tile rows, 1,023 of them each in its own 2 MB page along axis 0.
+// SFEM_MID_BLOCKED=0 turns it off (A/B).
+bool mid_tma_blocked(int n, int K) {
+  static const bool on = [] {
+    const char* e = std::getenv("SFEM_MID_BLOCKED");
+    return !(e && e[0] == '0');
+  }();
+  return on && mid_tma_enabled() && n == 1 && K == 1024;
+}
+
 cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
-                                 cudaStream_t stream) {
+                                 cudaStream_t stream, const void* smap) {
   if (geo.ntiles <= 0) return cudaSuccess;
   if (t.n == 1 && t.K == 1024)
-    return mid::launch_tma<1, 1024, SFEM_MID_B_N1, SFEM_MID_TH_N1>(t, tmap, geo, mode, analysis, stream);
+    return mid::launch_tma<1, 1024, SFEM_MID_B_N1, SFEM_MID_TH_N1>(t, tmap, geo, mode, analysis, stream, smap);
+  if (smap != nullptr && smap != tmap) return cudaErrorNotSupported;
   if (t.n == 2 && t.K == 512)
     return mid::launch_tma<2, 512, SFEM_MID_B_N2, SFEM_MID_TH_N2>(t, tmap, geo, mode, analysis, stream);
   if (t.n == 4 && t.K == 256)

@@ -1255,7 +1255,15 @@ __global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))  // <= 128 regis
     const long long l = l0 + b;
     const long long r = l / ls.ninner;
     off[b] = l < ls.nlines ? (r / ls.n1) * ls.os2 + (r % ls.n1) * ls.os1 + (l % ls.ninner) * ls.is : 0;
-    if (MODE == kForwardDivideInverse) {
+    if (MODE == kForwardDivideInverse && sym.xblk > 0) {
+      // blocked 3-D layout (capi.cu build_blocked_steps): row (x_hi, y, x_lo), x = x_hi*xblk + x_lo
+      const long long lb = l < ls.nlines ? l : 0;
+      const long long xlo = lb % sym.xblk, r1 = lb / sym.xblk;
+      const long long y = r1 % sym.lead_ext[1], xhi = r1 / sym.lead_ext[1];
+      const long long x = min(xhi * sym.xblk + xlo, sym.x_ext - 1);  // padding rows: any finite base
+      const double t0 = sym.lead_f[0] * sym.lead_eig[0][x], t1 = sym.lead_f[1] * sym.lead_eig[1][y];
+      base[b] = (sym.shift + t0) + t1;
+    } else if (MODE == kForwardDivideInverse) {
       // base = shift + sum_{i<N-1} f_i lambda_i (poisson.cpp:586-590 order)
       long long rem = l < ls.nlines ? l : 0;
       double terms[kMaxDim];
@@ -1426,8 +1434,8 @@ struct TmaShape {
 
 template <int NN, int K, int BB, int TH, int MODE>
 __global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))
-    sweep_mid_tma(DevTable t, const __grid_constant__ CUtensorMap tmap, TmaGeom geo, const double* __restrict__ mixF,
-                  const double* __restrict__ e0F) {
+    sweep_mid_tma(DevTable t, const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap smap,
+                  TmaGeom geo, const double* __restrict__ mixF, const double* __restrict__ e0F) {
   using C = Cfg<NN, K, BB, TH, false>;
   using TS = TmaShape<NN, K, BB, TH>;
   extern __shared__ __align__(128) double smem[];  // no static shared memory: the tile starts 128-byte aligned
@@ -1455,14 +1463,25 @@ __global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mid_smem_u32(bar)),
                  "r"(static_cast<unsigned>(TS::NBOX * TS::BOXP * BB * sizeof(double)))
                  : "memory");
-#pragma unroll 1
-    for (int j = 0; j < TS::NBOX; ++j)
+    // box coordinates (sweep.cuh BoxMode): plain {c0, j*boxp, c2, c3}; swept axis stored blocked: one box
+    // {BB, xblk, nhi, 1} at {c0, 0, 0, c2}; the tile's fixed coordinate blocked: {c0, j*boxp, c2 % xblk, c2 / xblk}
+    if (geo.ld_mode == kBoxSwept) {
       asm volatile(
           "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-          "[%6];\n" ::"r"(mid_smem_u32(R + j * TS::BOXP * BB)),
-          "l"(&tmap), "r"(c0), "r"(j * TS::BOXP), "r"(c2), "r"(c3), "r"(mid_smem_u32(bar))
+          "[%6];\n" ::"r"(mid_smem_u32(R)),
+          "l"(&tmap), "r"(c0), "r"(0), "r"(0), "r"(c2), "r"(mid_smem_u32(bar))
           : "memory");
-    if (geo.prefetch > 0) {
+    } else {
+      const int k2 = geo.ld_mode == kBoxSplit ? c2 % geo.xblk : c2, k3 = geo.ld_mode == kBoxSplit ? c2 / geo.xblk : c3;
+#pragma unroll 1
+      for (int j = 0; j < TS::NBOX; ++j)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+            "[%6];\n" ::"r"(mid_smem_u32(R + j * TS::BOXP * BB)),
+            "l"(&tmap), "r"(c0), "r"(j * TS::BOXP), "r"(k2), "r"(k3), "r"(mid_smem_u32(bar))
+            : "memory");
+    }
+    if (geo.prefetch > 0 && geo.ld_mode == kBoxPlain) {
       // L2 prefetch of the tile the next CTA on this SM will load (one resident
       // wave ahead).  Only for sweeps whose positions are a few KB apart: C5
       // n=4 axis-1 sweeps -6 %, but +22 % along axis 0, whose rows are planes
@@ -1511,11 +1530,18 @@ __global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) {
-#pragma unroll 1
-    for (int j = 0; j < TS::NBOX; ++j)
-      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(&tmap),
-                   "r"(c0), "r"(j * TS::BOXP), "r"(c2), "r"(c3), "r"(mid_smem_u32(R + j * TS::BOXP * BB))
+    if (geo.st_mode == kBoxSwept) {
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(&smap),
+                   "r"(c0), "r"(0), "r"(0), "r"(c2), "r"(mid_smem_u32(R))
                    : "memory");
+    } else {
+      const int k2 = geo.st_mode == kBoxSplit ? c2 % geo.xblk : c2, k3 = geo.st_mode == kBoxSplit ? c2 / geo.xblk : c3;
+#pragma unroll 1
+      for (int j = 0; j < TS::NBOX; ++j)
+        asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(&smap),
+                     "r"(c0), "r"(j * TS::BOXP), "r"(k2), "r"(k3), "r"(mid_smem_u32(R + j * TS::BOXP * BB))
+                     : "memory");
+    }
     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
   }
@@ -1525,7 +1551,7 @@ __global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))
 
 template <int NN, int K, int BB, int TH>
 cudaError_t launch_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, int mode, int analysis,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, const void* smap_in = nullptr) {
   using TS = TmaShape<NN, K, BB, TH>;
   if constexpr (!TS::OK) {
     return cudaErrorNotSupported;
@@ -1535,6 +1561,7 @@ cudaError_t launch_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, 
                                        : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
     const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
     const CUtensorMap* map = static_cast<const CUtensorMap*>(tmap);
+    const CUtensorMap* smap = smap_in ? static_cast<const CUtensorMap*>(smap_in) : map;  // in place: one map
     const long long ext3 = geo.ntiles / (geo.nblk0 * geo.ext2);
     const bool grid3 = geo.nblk0 < (1LL << 31) && geo.ext2 <= 65535 && ext3 <= 65535;
     const dim3 grid = grid3 ? dim3(static_cast<unsigned>(geo.nblk0), static_cast<unsigned>(geo.ext2),
@@ -1545,12 +1572,12 @@ cudaError_t launch_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, 
       auto kern = sweep_mid_tma<NN, K, BB, TH, kForward>;
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TS::SMEM));
       if (err != cudaSuccess) return err;
-      kern<<<grid, TH, TS::SMEM, stream>>>(t, *map, geo, mixF, e0F);
+      kern<<<grid, TH, TS::SMEM, stream>>>(t, *map, *smap, geo, mixF, e0F);
     } else {
       auto kern = sweep_mid_tma<NN, K, BB, TH, kInverse>;
       err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(TS::SMEM));
       if (err != cudaSuccess) return err;
-      kern<<<grid, TH, TS::SMEM, stream>>>(t, *map, geo, mixF, e0F);
+      kern<<<grid, TH, TS::SMEM, stream>>>(t, *map, *smap, geo, mixF, e0F);
     }
     return cudaGetLastError();
   }
