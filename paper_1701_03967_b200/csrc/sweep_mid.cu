@@ -249,7 +249,8 @@ cudaError_t launch_sweep_mid_tma_cm(const DevTable& t, const void* maps, const T
 
 // Shapes whose 3-D solves run the blocked schedule (capi.cu build_blocked_mid_steps): axis 0 stored as
 // (x_hi, y, x_lo, z) in a plan scratch, so an axis-0 tile's rows are 8-row groups instead of one row per plane.
-// n = 1, K = 1024 (C5): 32-byte tile rows, 1,023 of them each in its own 2 MB page along axis 0.
+// n = 1, K = 1024 (C5): 32-byte tile rows, 1,023 of them each in its own 2 MB page along axis 0.  Measured and left
+// off for n = 9, K = 114 (64-byte rows: 46.2 -> 46.8 ms, profiles/r4s_mid_blocked_n9_rejected.txt).
 // SFEM_MID_BLOCKED=0 turns it off (A/B).
 bool mid_tma_blocked(int n, int K) {
   static const bool on = [] {
@@ -264,13 +265,13 @@ cudaError_t launch_sweep_mid_tma(const DevTable& t, const void* tmap, const TmaG
   if (geo.ntiles <= 0) return cudaSuccess;
   if (t.n == 1 && t.K == 1024)
     return mid::launch_tma<1, 1024, SFEM_MID_B_N1, SFEM_MID_TH_N1>(t, tmap, geo, mode, analysis, stream, smap);
-  if (smap != nullptr && smap != tmap) return cudaErrorNotSupported;
   if (t.n == 2 && t.K == 512)
     return mid::launch_tma<2, 512, SFEM_MID_B_N2, SFEM_MID_TH_N2>(t, tmap, geo, mode, analysis, stream);
   if (t.n == 4 && t.K == 256)
     return mid::launch_tma<4, 256, SFEM_MID_B_N4, SFEM_MID_TH_N4>(t, tmap, geo, mode, analysis, stream);
   if (t.n == 9 && t.K == 114)
-    return mid::launch_tma<9, 114, SFEM_MID_B_N9, SFEM_MID_TH_N9>(t, tmap, geo, mode, analysis, stream);
+    return mid::launch_tma<9, 114, SFEM_MID_B_N9, SFEM_MID_TH_N9>(t, tmap, geo, mode, analysis, stream, smap);
+  if (smap != nullptr && smap != tmap) return cudaErrorNotSupported;
   if (t.n == 9 && t.K == 1024) return mid::launch_tma<9, 1024, 2, SFEM_MID_C3_TH>(t, tmap, geo, mode, analysis, stream);
 #if SFEM_MID_AUTO
   switch (t.K) {

@@ -1460,8 +1460,12 @@ __global__ void __launch_bounds__(TH, mid_min_blocks_n(NN, TH))
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mid_smem_u32(bar)), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mid_smem_u32(bar)),
-                 "r"(static_cast<unsigned>(TS::NBOX * TS::BOXP * BB * sizeof(double)))
+    // bytes of the tile's boxes; the one box of a blocked swept axis brings xblk * ceil(L / xblk) rows
+    const unsigned tile_bytes =
+        geo.ld_mode == kBoxSwept
+            ? static_cast<unsigned>((C::L + geo.xblk - 1) / geo.xblk * geo.xblk * BB * sizeof(double))
+            : static_cast<unsigned>(TS::NBOX * TS::BOXP * BB * sizeof(double));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mid_smem_u32(bar)), "r"(tile_bytes)
                  : "memory");
     // box coordinates (sweep.cuh BoxMode): plain {c0, j*boxp, c2, c3}; swept axis stored blocked: one box
     // {BB, xblk, nhi, 1} at {c0, 0, 0, c2}; the tile's fixed coordinate blocked: {c0, j*boxp, c2 % xblk, c2 / xblk}
@@ -1557,6 +1561,10 @@ cudaError_t launch_tma(const DevTable& t, const void* tmap, const TmaGeom& geo, 
     return cudaErrorNotSupported;
   } else {
     if (mode == kForwardDivideInverse || geo.nbox != TS::NBOX || geo.boxp != TS::BOXP) return cudaErrorInvalidValue;
+    using C = Cfg<NN, K, BB, TH, false>;
+    if ((geo.ld_mode == kBoxSwept || geo.st_mode == kBoxSwept) &&
+        (geo.xblk <= 0 || (C::L + geo.xblk - 1) / geo.xblk * geo.xblk * BB > C::REGION))
+      return cudaErrorInvalidValue;
     const double* mixF = SFEM_MID_KMIX ? (analysis == kDirect ? t.mixT_d : t.mixT_w)
                                        : (analysis == kDirect ? t.mix_fwd_d : t.mix_fwd_w);
     const double* e0F = analysis == kDirect ? t.e0_fwd_d : t.e0_fwd_w;
