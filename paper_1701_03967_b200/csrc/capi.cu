@@ -742,12 +742,22 @@ void build_blocked_steps(sfem_plan_s* p, long long pitch) {
 
 // The same schedule for the mid kernels (sweep_mid_tma with box modes, sweep_mid rows with the blocked row
 // order in the symbol): shapes mid_tma_blocked() names, all three axes on one table.
+// rows per group of the blocked axis in the mid schedule (SFEM_MID_XBLK: A/B)
+long long mid_xblk() {
+  static const long long v = [] {
+    const char* e = std::getenv("SFEM_MID_XBLK");
+    const long long x = e ? std::atoll(e) : 0;
+    return (x >= 2 && x <= 256) ? x : static_cast<long long>(kXBlk);
+  }();
+  return v;
+}
+
 bool blocked_mid_ok(const sfem_plan_s* p, long long pitch) {
   if (p->dim != 3 || !p->use_fast || std::getenv("SFEM_PLAIN")) return false;
   const DevTable& t0 = p->tables[0]->dev;
   if (p->tables[1] != p->tables[0] || p->tables[2] != p->tables[0]) return false;
   if (!mid_tma_blocked(t0.n, t0.K) || mid_tma_lines(t0.n, t0.K) <= 0 || mid_tma_cm(t0.n, t0.K)) return false;
-  const long long nhi = (p->ext[0] + kXBlk - 1) / kXBlk;
+  const long long nhi = (p->ext[0] + mid_xblk() - 1) / mid_xblk();
   const long long tb = mid_tma_lines(t0.n, t0.K), nbox = (p->ext[0] + 255) / 256;
   const long long balign = tb % 16 == 0 ? 1 : (tb % 8 == 0 ? 2 : (tb % 4 == 0 ? 4 : (tb % 2 == 0 ? 8 : 16)));
   const long long boxp = ((p->ext[0] + nbox - 1) / nbox + balign - 1) / balign * balign;  // as strided_step
@@ -759,7 +769,7 @@ bool blocked_mid_ok(const sfem_plan_s* p, long long pitch) {
 
 void build_blocked_mid_steps(sfem_plan_s* p, long long pitch) {
   const long long L0 = p->ext[0], L1 = p->ext[1], L2 = p->ext[2];
-  const long long bp = (L2 + 3) & ~3LL, X = kXBlk, nhi = (L0 + X - 1) / X;
+  const long long bp = (L2 + 3) & ~3LL, X = mid_xblk(), nhi = (L0 + X - 1) / X;
   p->bpitch = bp;
   p->belems = static_cast<size_t>(nhi) * X * L1 * bp;
   const View v = plan_view(p, pitch);
