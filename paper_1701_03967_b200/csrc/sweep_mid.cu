@@ -54,6 +54,40 @@ extern template cudaError_t launch_auto_n<768>(const DevTable&, const LineSet&, 
                                                   cudaStream_t);
 extern template cudaError_t launch_auto_n<1000>(const DevTable&, const LineSet&, int, int, const SymbolInfo*,
                                                   cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<16>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<24>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<32>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<40>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<48>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<64>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<80>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<96>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<100>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<128>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<160>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<192>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<200>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<256>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<320>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<384>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
+extern template cudaError_t launch_auto_tma_cm_n<512>(const DevTable&, const void*, const TmaGeom&, int, int,
+                                                        cudaStream_t);
 extern template cudaError_t launch_auto_tma_n<16>(const DevTable&, const void*, const TmaGeom&, int, int,
                                                      cudaStream_t);
 extern template cudaError_t launch_auto_tma_n<24>(const DevTable&, const void*, const TmaGeom&, int, int,
@@ -229,7 +263,32 @@ bool mid_tma_cm(int n, int K) {
     return !(e && e[0] == '0');
   }();
   if (!on || !mid_tma_enabled()) return false;
-  return (n == 4 && K == 256 && SFEM_MID_B_N4 == 8) || (n == 2 && K == 512 && SFEM_MID_B_N2 == 8);
+  if ((n == 4 && K == 256 && SFEM_MID_B_N4 == 8) || (n == 2 && K == 512 && SFEM_MID_B_N2 == 8)) return true;
+#if SFEM_MID_AUTO
+  if (!mid_auto(n, K)) return false;
+  switch (K) {
+    case 16: return mid::auto_tma_cm_n<16>(n);
+    case 24: return mid::auto_tma_cm_n<24>(n);
+    case 32: return mid::auto_tma_cm_n<32>(n);
+    case 40: return mid::auto_tma_cm_n<40>(n);
+    case 48: return mid::auto_tma_cm_n<48>(n);
+    case 64: return mid::auto_tma_cm_n<64>(n);
+    case 80: return mid::auto_tma_cm_n<80>(n);
+    case 96: return mid::auto_tma_cm_n<96>(n);
+    case 100: return mid::auto_tma_cm_n<100>(n);
+    case 128: return mid::auto_tma_cm_n<128>(n);
+    case 160: return mid::auto_tma_cm_n<160>(n);
+    case 192: return mid::auto_tma_cm_n<192>(n);
+    case 200: return mid::auto_tma_cm_n<200>(n);
+    case 256: return mid::auto_tma_cm_n<256>(n);
+    case 320: return mid::auto_tma_cm_n<320>(n);
+    case 384: return mid::auto_tma_cm_n<384>(n);
+    case 512: return mid::auto_tma_cm_n<512>(n);
+    default: return false;
+  }
+#else
+  return false;
+#endif
 #else
   (void)n;
   (void)K;
@@ -243,6 +302,28 @@ cudaError_t launch_sweep_mid_tma_cm(const DevTable& t, const void* maps, const T
 #if SFEM_MID_CM
   if (t.n == 4 && t.K == 256) return mid::launch_tma_cm<4, 256, 8, SFEM_MID_TH_N4>(t, maps, geo, mode, analysis, stream);
   if (t.n == 2 && t.K == 512) return mid::launch_tma_cm<2, 512, 8, SFEM_MID_TH_N2>(t, maps, geo, mode, analysis, stream);
+#if SFEM_MID_AUTO
+  switch (t.K) {
+    case 16: return mid::launch_auto_tma_cm_n<16>(t, maps, geo, mode, analysis, stream);
+    case 24: return mid::launch_auto_tma_cm_n<24>(t, maps, geo, mode, analysis, stream);
+    case 32: return mid::launch_auto_tma_cm_n<32>(t, maps, geo, mode, analysis, stream);
+    case 40: return mid::launch_auto_tma_cm_n<40>(t, maps, geo, mode, analysis, stream);
+    case 48: return mid::launch_auto_tma_cm_n<48>(t, maps, geo, mode, analysis, stream);
+    case 64: return mid::launch_auto_tma_cm_n<64>(t, maps, geo, mode, analysis, stream);
+    case 80: return mid::launch_auto_tma_cm_n<80>(t, maps, geo, mode, analysis, stream);
+    case 96: return mid::launch_auto_tma_cm_n<96>(t, maps, geo, mode, analysis, stream);
+    case 100: return mid::launch_auto_tma_cm_n<100>(t, maps, geo, mode, analysis, stream);
+    case 128: return mid::launch_auto_tma_cm_n<128>(t, maps, geo, mode, analysis, stream);
+    case 160: return mid::launch_auto_tma_cm_n<160>(t, maps, geo, mode, analysis, stream);
+    case 192: return mid::launch_auto_tma_cm_n<192>(t, maps, geo, mode, analysis, stream);
+    case 200: return mid::launch_auto_tma_cm_n<200>(t, maps, geo, mode, analysis, stream);
+    case 256: return mid::launch_auto_tma_cm_n<256>(t, maps, geo, mode, analysis, stream);
+    case 320: return mid::launch_auto_tma_cm_n<320>(t, maps, geo, mode, analysis, stream);
+    case 384: return mid::launch_auto_tma_cm_n<384>(t, maps, geo, mode, analysis, stream);
+    case 512: return mid::launch_auto_tma_cm_n<512>(t, maps, geo, mode, analysis, stream);
+    default: break;
+  }
+#endif
 #endif
   return cudaErrorNotSupported;
 }

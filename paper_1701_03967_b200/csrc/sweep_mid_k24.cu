@@ -6,5 +6,6 @@ namespace sfem_b200 {
 namespace mid {
 template cudaError_t launch_auto_n<24>(const DevTable&, const LineSet&, int, int, const SymbolInfo*, cudaStream_t);
 template cudaError_t launch_auto_tma_n<24>(const DevTable&, const void*, const TmaGeom&, int, int, cudaStream_t);
+template cudaError_t launch_auto_tma_cm_n<24>(const DevTable&, const void*, const TmaGeom&, int, int, cudaStream_t);
 }  // namespace mid
 }  // namespace sfem_b200
